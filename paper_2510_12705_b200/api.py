@@ -1,0 +1,149 @@
+"""Torch-facing convenience layer over the C ABI (marshalling only).
+
+Tensors are device memory; the work runs on ``torch.cuda.current_stream()``.
+Every step of the reduction runs in the CUDA kernels behind
+``libbandbidiag.so``; nothing here computes.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _native as N
+
+_DT = {torch.float16: N.BB_F16, torch.float32: N.BB_F32, torch.float64: N.BB_F64}
+_DT_NAME = {"f16": torch.float16, "f32": torch.float32, "f64": torch.float64}
+
+
+def bb_dtype(t) -> int:
+    if isinstance(t, str):
+        t = _DT_NAME[t]
+    if isinstance(t, torch.Tensor):
+        t = t.dtype
+    if t not in _DT:
+        raise N.BBError(N.BB_ERR_NOT_SUPPORTED, f"dtype {t}")
+    return _DT[t]
+
+
+@dataclass
+class Config:
+    """The paper's hyperparameter triple plus scheduling knobs."""
+    tw: int = 0
+    threads_per_block: int = 0
+    max_blocks_per_sm: int = 0
+    dep_distance: int = 0
+    schedule: int = N.BB_SCHED_AUTO
+    nonneg: bool = False
+
+    def c(self) -> N.bb_config:
+        return N.bb_config(self.tw, self.threads_per_block, self.max_blocks_per_sm, self.dep_distance,
+                           self.schedule, N.BB_FLAG_NONNEG_OUTPUT if self.nonneg else 0)
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _cfg(cfg: Config | None, tw: int | None) -> Config:
+    cfg = Config() if cfg is None else Config(**cfg.__dict__)
+    if tw is not None:
+        cfg.tw = int(tw)
+    return cfg
+
+
+def plan(n: int, b: int, dtype="f64", batch: int = 1, cfg: Config | None = None, tw: int | None = None) -> dict:
+    return N.bb_plan(n, b, bb_dtype(dtype), batch, _cfg(cfg, tw).c())
+
+
+def launch_count(n: int, b: int, dtype="f64", batch: int = 1, cfg: Config | None = None,
+                 tw: int | None = None) -> int:
+    return N.bb_launch_count(n, b, bb_dtype(dtype), batch, _cfg(cfg, tw).c())
+
+
+class Workspace:
+    """Pre-allocated device workspace for the _ex entry points (timing excludes
+    allocation).  ``band_view()`` exposes the working band (documented layout)."""
+
+    def __init__(self, n: int, b: int, dtype, batch: int = 1, cfg: Config | None = None,
+                 tw: int | None = None, device=None):
+        self.n, self.b, self.batch = n, b, batch
+        self.dtype = _DT_NAME[dtype] if isinstance(dtype, str) else dtype
+        self.cfg = _cfg(cfg, tw)
+        self.stats = plan(n, b, self.dtype, batch, self.cfg)
+        self.nbytes = self.stats["workspace_bytes"]
+        self.buf = torch.empty(max(self.nbytes, 1), dtype=torch.uint8,
+                               device=device if device is not None else "cuda")
+
+    def band_view(self) -> torch.Tensor:
+        """Working band after a call: shape (batch, n, ldw), [k, j, ku + i - j] = A_k(i, j)."""
+        es = torch.empty(0, dtype=self.dtype).element_size()
+        cnt = self.batch * self.n * self.stats["ldw"]
+        return self.buf[: cnt * es].view(self.dtype).view(self.batch, self.n, self.stats["ldw"])
+
+
+def band_to_bidiag(band: torch.Tensor, b: int, tw: int | None = None, cfg: Config | None = None,
+                   workspace: Workspace | None = None, out=None):
+    """Reduce one upper-banded matrix.  ``band``: CUDA tensor (n, ldband),
+    ``band[j, b + i - j] = A[i, j]`` (LAPACK upper band).  Returns (d, e)."""
+    if band.dim() != 2 or not band.is_cuda:
+        raise ValueError("band must be a 2-D CUDA tensor (n, ldband)")
+    band = band.contiguous()
+    n, ld = band.shape
+    dt = bb_dtype(band)
+    if out is None:
+        d = torch.empty(n, dtype=band.dtype, device=band.device)
+        e = torch.empty(max(n - 1, 0), dtype=band.dtype, device=band.device)
+    else:
+        d, e = out
+    c = _cfg(cfg, tw)
+    if workspace is None and c == Config():
+        N.bb_band_to_bidiag(n, b, dt, band.data_ptr(), ld, d.data_ptr(), e.data_ptr(), _stream())
+    elif workspace is None:
+        ws = Workspace(n, b, band.dtype, 1, c, device=band.device)
+        N.bb_band_to_bidiag_ex(n, b, dt, band.data_ptr(), ld, d.data_ptr(), e.data_ptr(), c.c(),
+                               ws.buf.data_ptr(), ws.nbytes, _stream())
+    else:
+        N.bb_band_to_bidiag_ex(n, b, dt, band.data_ptr(), ld, d.data_ptr(), e.data_ptr(), workspace.cfg.c(),
+                               workspace.buf.data_ptr(), workspace.nbytes, _stream())
+    return d, e
+
+
+def band_to_bidiag_batched(band: torch.Tensor, b: int, tw: int | None = None, cfg: Config | None = None,
+                           workspace: Workspace | None = None, out=None):
+    """Reduce ``batch`` independent matrices ``band``: (batch, n, ldband)."""
+    if band.dim() != 3 or not band.is_cuda:
+        raise ValueError("band must be a 3-D CUDA tensor (batch, n, ldband)")
+    band = band.contiguous()
+    B, n, ld = band.shape
+    dt = bb_dtype(band)
+    if out is None:
+        d = torch.empty(B, n, dtype=band.dtype, device=band.device)
+        e = torch.empty(B, max(n - 1, 1), dtype=band.dtype, device=band.device)
+    else:
+        d, e = out
+    c = _cfg(cfg, tw) if workspace is None else workspace.cfg
+    ws = workspace if workspace is not None else Workspace(n, b, band.dtype, B, c, device=band.device)
+    N.bb_band_to_bidiag_batched_ex(n, b, dt, B, band.data_ptr(), ld, n * ld, d.data_ptr(), d.stride(0),
+                                   e.data_ptr(), e.stride(0), c.c(), ws.buf.data_ptr(), ws.nbytes, _stream())
+    return d, e[:, : max(n - 1, 0)]
+
+
+def band_to_bidiag_host(band, b: int, tw: int | None = None, cfg: Config | None = None):
+    """End-to-end from HOST memory (numpy array or CPU tensor, (n, ld) or
+    (batch, n, ld)): H2D copy, reduction, D2H copy inside the C ABI call.
+    Blocks until the host results are valid."""
+    t = torch.as_tensor(band)
+    if t.is_cuda:
+        raise ValueError("band_to_bidiag_host takes host memory")
+    t = t.contiguous()
+    single = t.dim() == 2
+    if single:
+        t = t.unsqueeze(0)
+    B, n, ld = t.shape
+    d = torch.empty(B, n, dtype=t.dtype, pin_memory=t.is_pinned())
+    e = torch.empty(B, max(n - 1, 1), dtype=t.dtype, pin_memory=t.is_pinned())
+    N.bb_band_to_bidiag_host(n, b, bb_dtype(t), B, t.data_ptr(), ld, n * ld, d.data_ptr(), d.stride(0),
+                             e.data_ptr(), e.stride(0), _cfg(cfg, tw).c(), _stream())
+    e = e[:, : max(n - 1, 0)]
+    return (d[0], e[0]) if single else (d, e)

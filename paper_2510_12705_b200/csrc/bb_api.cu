@@ -1,0 +1,460 @@
+// bb_api.cu -- C ABI (include/bandbidiag.h) of the B200 band -> bidiagonal
+// reduction: argument validation, pass plan (Alg. 1 line 1), workspace
+// carving, and the launch sequence pack -> one launch per pass -> extract.
+//
+// Host logic only; every arithmetic step of the method runs in the kernels of
+// bb_kernels.cuh.  No CPU fallback exists: without a usable CUDA device every
+// compute entry point returns BB_ERR_CUDA.
+#include "bb_kernels.cuh"
+#include "bandbidiag.h"
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+namespace {
+
+constexpr size_t kAlign = 256;
+constexpr int kSmemOptinFallback = 227 * 1024;
+
+inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+inline int round_odd(int x) { return (x & 1) ? x : x + 1; }
+
+size_t elem_size(bb_dtype dt)
+{
+    switch (dt) {
+    case BB_F16: return 2;
+    case BB_F32: return 4;
+    case BB_F64: return 8;
+    }
+    return 0;
+}
+size_t compute_size(bb_dtype dt) { return dt == BB_F64 ? 8 : 4; }
+
+struct PassPlan {
+    int c, t, s;
+    int nsweeps;     // non-empty sweeps: r in [0, nsweeps)
+    int cycles;      // max_r (s*r + J_r)
+    int LT, LW;
+    size_t smem;     // dynamic shared memory bytes
+    int threads;
+};
+
+struct Plan {
+    int64_t n = 0, b_eff = 0, batch = 0;
+    int tw = 0;
+    int64_t ldw = 0, ku = 0;
+    bb_config cfg{};
+    std::vector<PassPlan> passes;
+    size_t band_bytes = 0, flag_bytes = 0, counter_bytes = 0, total = 0;
+};
+
+int default_tw(bb_dtype dt)
+{
+    // optimum = one 128-byte cache line: 32 (FP32), 16 (FP64).
+    return dt == BB_F64 ? 16 : 32;
+}
+
+int64_t sweep_len_h(int64_t n, int64_t c, int64_t t, int64_t r)
+{
+    int64_t first = r + c - t;
+    return first > n - 2 ? 0 : (n - 2 - first) / c + 1;
+}
+
+bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const bb_config *cfg_in, Plan &P)
+{
+    if (elem_size(dtype) == 0) return BB_ERR_NOT_SUPPORTED;
+    if (n < 0 || b < 0 || batch < 0) return BB_ERR_INVALID_VALUE;
+    bb_config cfg{};
+    if (cfg_in) cfg = *cfg_in;
+    if (cfg.tw < 0 || cfg.threads_per_block < 0 || cfg.max_blocks_per_sm < 0 || cfg.dep_distance < 0 ||
+        cfg.schedule < 0 || cfg.schedule > BB_SCHED_CYCLE)
+        return BB_ERR_INVALID_VALUE;
+    if (cfg.threads_per_block && (cfg.threads_per_block % 32 || cfg.threads_per_block > 512))
+        return BB_ERR_INVALID_VALUE;
+    if (cfg.schedule == BB_SCHED_AUTO) cfg.schedule = BB_SCHED_FLAGS;
+    P.n = n;
+    P.batch = batch;
+    P.b_eff = n > 0 ? std::min<int64_t>(b, n - 1) : 0;
+    int tw = cfg.tw ? cfg.tw : default_tw(dtype);
+    // the headroom only needs the largest tilewidth any pass uses
+    tw = (int)std::max<int64_t>(1, std::min<int64_t>(tw, std::max<int64_t>(P.b_eff - 1, 1)));
+    cfg.tw = tw;
+    P.tw = tw;
+    P.ku = P.b_eff + tw;
+    P.ldw = P.b_eff + 2 * tw + 1; // band + twice the tilewidth (reading Q11)
+    P.passes.clear();
+    if (n > 2 && P.b_eff > 1) {
+        int64_t c = P.b_eff;
+        while (c > 1) {
+            int64_t t = std::min<int64_t>(tw, c - 1);
+            PassPlan pp{};
+            pp.c = (int)c;
+            pp.t = (int)t;
+            int s_auto = (c - t == 1) ? 3 : 2; // reading Q4
+            pp.s = std::max(s_auto, (int)cfg.dep_distance);
+            int64_t ns = std::max<int64_t>(0, (n - 2) - (c - t) + 1);
+            pp.nsweeps = (int)ns;
+            int64_t cyc = 0;
+            for (int64_t r = 0; r < ns; ++r) cyc = std::max(cyc, pp.s * r + sweep_len_h(n, c, t, r));
+            pp.cycles = (int)cyc;
+            pp.LT = round_odd((int)(c + t + 1));
+            pp.LW = round_odd((int)(t + 1));
+            size_t cs = compute_size(dtype);
+            pp.smem = ((size_t)pp.LT * (t + 1) + (size_t)pp.LW * c + (t + 1) + 8) * cs;
+            if (pp.smem > (size_t)kSmemOptinFallback) return BB_ERR_NOT_SUPPORTED;
+            int thr = cfg.threads_per_block;
+            if (!thr) thr = (int)std::min<int64_t>(256, std::max<int64_t>(64, (c + t + 31) / 32 * 32));
+            pp.threads = thr;
+            P.passes.push_back(pp);
+            c -= t;
+        }
+    }
+    P.cfg = cfg;
+    size_t es = elem_size(dtype);
+    P.band_bytes = align_up((size_t)batch * (size_t)n * (size_t)P.ldw * es);
+    P.flag_bytes = align_up((size_t)P.passes.size() * (size_t)batch * (size_t)n * sizeof(int));
+    P.counter_bytes = align_up(std::max<size_t>(1, P.passes.size()) * sizeof(int));
+    P.total = P.band_bytes + P.flag_bytes + P.counter_bytes;
+    return BB_SUCCESS;
+}
+
+struct DeviceInfo {
+    int sms = 0;
+    int smem_optin = 0;
+    bool ok = false;
+};
+
+bool device_info(DeviceInfo &out)
+{
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    static std::mutex mu;
+    static std::vector<DeviceInfo> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    if ((int)cache.size() <= dev) cache.resize(dev + 1);
+    if (!cache[dev].ok) {
+        DeviceInfo di;
+        if (cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&di.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        di.ok = true;
+        cache[dev] = di;
+    }
+    out = cache[dev];
+    return true;
+}
+
+template <class S>
+bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t stride_band, int64_t b_in,
+                     void *d_out, int64_t stride_d, void *e_out, int64_t stride_e, void *ws, cudaStream_t st)
+{
+    DeviceInfo di;
+    if (!device_info(di)) return BB_ERR_CUDA;
+    unsigned char *base = reinterpret_cast<unsigned char *>(ws);
+    S *W = reinterpret_cast<S *>(base);
+    int *flags = reinterpret_cast<int *>(base + P.band_bytes);
+    int *counters = reinterpret_cast<int *>(base + P.band_bytes + P.flag_bytes);
+    const int64_t mat_stride = P.n * P.ldw;
+    const int n = (int)P.n;
+    const int batch = (int)P.batch;
+
+    if (!P.passes.empty()) {
+        if (cudaMemsetAsync(flags, 0, P.flag_bytes + P.counter_bytes, st) != cudaSuccess) return BB_ERR_CUDA;
+    }
+    {
+        int64_t total = (int64_t)batch * mat_stride;
+        int thr = 256;
+        int64_t blocks = std::min<int64_t>((total + thr - 1) / thr, (int64_t)di.sms * 16);
+        bb::pack_kernel<S><<<(unsigned)std::max<int64_t>(blocks, 1), thr, 0, st>>>(
+            reinterpret_cast<const S *>(band), ldband, stride_band, (int)b_in, (int)P.b_eff, W, mat_stride,
+            (int)P.ldw, (int)P.ku, n, batch);
+    }
+    for (size_t pi = 0; pi < P.passes.size(); ++pi) {
+        const PassPlan &pp = P.passes[pi];
+        if ((int)pp.smem > di.smem_optin) return BB_ERR_NOT_SUPPORTED;
+        bb::PassArgs a{};
+        a.W = W;
+        a.mat_stride = mat_stride;
+        a.ldw = (int)P.ldw;
+        a.ku = (int)P.ku;
+        a.n = n;
+        a.c = pp.c;
+        a.t = pp.t;
+        a.s = pp.s;
+        a.batch = batch;
+        a.nsweeps = pp.nsweeps;
+        a.progress = flags + (int64_t)pi * batch * n;
+        a.counter = counters + pi;
+        a.LT = pp.LT;
+        a.LW = pp.LW;
+        if (P.cfg.schedule == BB_SCHED_CYCLE) {
+            auto kern = bb::pass_cycle_kernel<S>;
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem) != cudaSuccess)
+                return BB_ERR_CUDA;
+            int maxT = pp.cycles;
+            if (const char *dbg = getenv("BB_DEBUG_MAX_CYCLES")) maxT = std::min(maxT, atoi(dbg)); // debug only
+            for (int T = 0; T < maxT; ++T) {
+                a.cycle_T = T;
+                int rmax = std::min(T / pp.s + 1, pp.nsweeps);
+                dim3 grid((unsigned)std::max(rmax, 1), (unsigned)batch);
+                kern<<<grid, pp.threads, pp.smem, st>>>(a);
+            }
+        } else {
+            auto kern = bb::pass_flags_kernel<S>;
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem) != cudaSuccess)
+                return BB_ERR_CUDA;
+            int occ = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, pp.threads, pp.smem) != cudaSuccess)
+                return BB_ERR_CUDA;
+            if (P.cfg.max_blocks_per_sm > 0) occ = std::min(occ, (int)P.cfg.max_blocks_per_sm);
+            occ = std::max(occ, 1);
+            int64_t tasks = (int64_t)pp.nsweeps * batch;
+            int64_t grid = std::min<int64_t>(tasks, (int64_t)occ * di.sms);
+            if (grid < 1) continue;
+            kern<<<(unsigned)grid, pp.threads, pp.smem, st>>>(a);
+        }
+        if (cudaGetLastError() != cudaSuccess) return BB_ERR_CUDA;
+    }
+    {
+        int64_t total = (int64_t)batch * n;
+        int thr = 256;
+        int64_t blocks = std::min<int64_t>((total + thr - 1) / thr, (int64_t)di.sms * 8);
+        bb::extract_kernel<S><<<(unsigned)std::max<int64_t>(blocks, 1), thr, 0, st>>>(
+            W, mat_stride, (int)P.ldw, (int)P.ku, n, batch, reinterpret_cast<S *>(d_out), stride_d,
+            reinterpret_cast<S *>(e_out), stride_e, (P.cfg.flags & BB_FLAG_NONNEG_OUTPUT) ? 1 : 0);
+    }
+    if (cudaGetLastError() != cudaSuccess) return BB_ERR_CUDA;
+    return BB_SUCCESS;
+}
+
+bb_status validate(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const void *band, int64_t ldband,
+                   int64_t stride_band, const void *d_out, int64_t stride_d, const void *e_out, int64_t stride_e)
+{
+    if (elem_size(dtype) == 0) return BB_ERR_NOT_SUPPORTED;
+    if (n < 0 || b < 0 || batch < 0) return BB_ERR_INVALID_VALUE;
+    if (ldband < b + 1) return BB_ERR_INVALID_VALUE;
+    if (n == 0 || batch == 0) return BB_SUCCESS;
+    if (!band || !d_out || (n > 1 && !e_out)) return BB_ERR_INVALID_VALUE;
+    if (batch > 1) {
+        if (stride_band < n * ldband || stride_d < n || stride_e < n - 1) return BB_ERR_INVALID_VALUE;
+    }
+    if (n > INT32_MAX / 4 || ldband > INT32_MAX || b > INT32_MAX / 4) return BB_ERR_NOT_SUPPORTED;
+    return BB_SUCCESS;
+}
+
+bb_status run_ex(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const void *band, int64_t ldband,
+                 int64_t stride_band, void *d_out, int64_t stride_d, void *e_out, int64_t stride_e,
+                 const bb_config *cfg, void *ws, size_t ws_bytes, cudaStream_t st)
+{
+    bb_status v = validate(n, b, dtype, batch, band, ldband, stride_band, d_out, stride_d, e_out, stride_e);
+    if (v != BB_SUCCESS) return v;
+    Plan P;
+    bb_status s = make_plan(n, b, dtype, batch, cfg, P);
+    if (s != BB_SUCCESS) return s;
+    if (n == 0 || batch == 0) return BB_SUCCESS;
+    if (!ws || ws_bytes < P.total) return BB_ERR_INVALID_VALUE;
+    switch (dtype) {
+    case BB_F16: return launch_all<__half>(P, band, ldband, stride_band, b, d_out, stride_d, e_out, stride_e, ws, st);
+    case BB_F32: return launch_all<float>(P, band, ldband, stride_band, b, d_out, stride_d, e_out, stride_e, ws, st);
+    case BB_F64: return launch_all<double>(P, band, ldband, stride_band, b, d_out, stride_d, e_out, stride_e, ws, st);
+    }
+    return BB_ERR_NOT_SUPPORTED;
+}
+
+bb_status run_alloc(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const void *band, int64_t ldband,
+                    int64_t stride_band, void *d_out, int64_t stride_d, void *e_out, int64_t stride_e,
+                    const bb_config *cfg, cudaStream_t st)
+{
+    bb_status v = validate(n, b, dtype, batch, band, ldband, stride_band, d_out, stride_d, e_out, stride_e);
+    if (v != BB_SUCCESS) return v;
+    Plan P;
+    bb_status s = make_plan(n, b, dtype, batch, cfg, P);
+    if (s != BB_SUCCESS) return s;
+    if (n == 0 || batch == 0) return BB_SUCCESS;
+    void *ws = nullptr;
+    cudaError_t e = cudaMallocAsync(&ws, P.total, st);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        return BB_ERR_OUT_OF_MEMORY;
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return BB_ERR_CUDA;
+    }
+    s = run_ex(n, b, dtype, batch, band, ldband, stride_band, d_out, stride_d, e_out, stride_e, cfg, ws, P.total, st);
+    if (cudaFreeAsync(ws, st) != cudaSuccess && s == BB_SUCCESS) s = BB_ERR_CUDA;
+    return s;
+}
+
+} // namespace
+
+extern "C" {
+
+bb_status bb_band_to_bidiag(int64_t n, int64_t b, bb_dtype dtype, const void *band, int64_t ldband, void *d_out,
+                            void *e_out, void *stream)
+{
+    return run_alloc(n, b, dtype, 1, band, ldband, n * ldband, d_out, n, e_out, n - 1, nullptr,
+                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+bb_status bb_band_to_bidiag_batched(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const void *band,
+                                    int64_t ldband, int64_t stride_band, void *d_out, int64_t stride_d, void *e_out,
+                                    int64_t stride_e, void *stream)
+{
+    return run_alloc(n, b, dtype, batch, band, ldband, stride_band, d_out, stride_d, e_out, stride_e, nullptr,
+                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+bb_status bb_band_to_bidiag_ex(int64_t n, int64_t b, bb_dtype dtype, const void *band, int64_t ldband, void *d_out,
+                               void *e_out, const bb_config *cfg, void *workspace, size_t workspace_bytes,
+                               void *stream)
+{
+    return run_ex(n, b, dtype, 1, band, ldband, n * ldband, d_out, n, e_out, n - 1, cfg, workspace, workspace_bytes,
+                  reinterpret_cast<cudaStream_t>(stream));
+}
+
+bb_status bb_band_to_bidiag_batched_ex(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const void *band,
+                                       int64_t ldband, int64_t stride_band, void *d_out, int64_t stride_d,
+                                       void *e_out, int64_t stride_e, const bb_config *cfg, void *workspace,
+                                       size_t workspace_bytes, void *stream)
+{
+    return run_ex(n, b, dtype, batch, band, ldband, stride_band, d_out, stride_d, e_out, stride_e, cfg, workspace,
+                  workspace_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
+bb_status bb_band_to_bidiag_host(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const void *band_host,
+                                 int64_t ldband, int64_t stride_band, void *d_host, int64_t stride_d, void *e_host,
+                                 int64_t stride_e, const bb_config *cfg, void *stream)
+{
+    if (batch == 1) {
+        stride_band = n * ldband;
+        stride_d = n;
+        stride_e = n - 1;
+    }
+    bb_status v = validate(n, b, dtype, batch, band_host, ldband, stride_band, d_host, stride_d, e_host, stride_e);
+    if (v != BB_SUCCESS) return v;
+    Plan P;
+    bb_status s = make_plan(n, b, dtype, batch, cfg, P);
+    if (s != BB_SUCCESS) return s;
+    if (n == 0 || batch == 0) return BB_SUCCESS;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const size_t es = elem_size(dtype);
+    const size_t band_b = align_up((size_t)batch * stride_band * es);
+    const size_t d_b = align_up((size_t)batch * stride_d * es);
+    const size_t e_b = align_up((size_t)batch * std::max<int64_t>(stride_e, 1) * es);
+    unsigned char *buf = nullptr;
+    const size_t total = band_b + d_b + e_b + P.total;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&buf), total, st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return e == cudaErrorMemoryAllocation ? BB_ERR_OUT_OF_MEMORY : BB_ERR_CUDA;
+    }
+    void *dband = buf, *dd = buf + band_b, *de = buf + band_b + d_b, *ws = buf + band_b + d_b + e_b;
+    const size_t in_bytes = (size_t)((batch - 1) * stride_band + n * ldband) * es;
+    if (cudaMemcpyAsync(dband, band_host, in_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) s = BB_ERR_CUDA;
+    if (s == BB_SUCCESS)
+        s = run_ex(n, b, dtype, batch, dband, ldband, stride_band, dd, stride_d, de, stride_e, cfg, ws, P.total, st);
+    if (s == BB_SUCCESS) {
+        const size_t dn = (size_t)((batch - 1) * stride_d + n) * es;
+        if (cudaMemcpyAsync(d_host, dd, dn, cudaMemcpyDeviceToHost, st) != cudaSuccess) s = BB_ERR_CUDA;
+        if (n > 1) {
+            const size_t en = (size_t)((batch - 1) * stride_e + (n - 1)) * es;
+            if (cudaMemcpyAsync(e_host, de, en, cudaMemcpyDeviceToHost, st) != cudaSuccess) s = BB_ERR_CUDA;
+        }
+    }
+    if (cudaFreeAsync(buf, st) != cudaSuccess && s == BB_SUCCESS) s = BB_ERR_CUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess && s == BB_SUCCESS) s = BB_ERR_CUDA;
+    return s;
+}
+
+bb_status bb_workspace_size(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const bb_config *cfg, size_t *bytes)
+{
+    if (!bytes) return BB_ERR_INVALID_VALUE;
+    Plan P;
+    bb_status s = make_plan(n, b, dtype, batch, cfg, P);
+    if (s != BB_SUCCESS) return s;
+    *bytes = P.total;
+    return BB_SUCCESS;
+}
+
+bb_status bb_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const bb_config *cfg, bb_plan_stats *out)
+{
+    if (!out) return BB_ERR_INVALID_VALUE;
+    Plan P;
+    bb_status s = make_plan(n, b, dtype, batch, cfg, P);
+    if (s != BB_SUCCESS) return s;
+    std::memset(out, 0, sizeof(*out));
+    out->passes = (int64_t)P.passes.size();
+    out->tw = P.tw;
+    out->ldw = P.ldw;
+    out->ku = P.ku;
+    out->workspace_bytes = P.total;
+    out->threads_per_block = P.passes.empty() ? 0 : P.passes[0].threads;
+    double elems = 0, flops = 0;
+    int64_t steps = 0, crit = 0;
+    for (const PassPlan &pp : P.passes) {
+        crit += pp.cycles;
+        for (int64_t r = 0; r < pp.nsweeps; ++r) {
+            int64_t J = sweep_len_h(n, pp.c, pp.t, r);
+            for (int64_t j = 0; j < J; ++j) {
+                int64_t p = r + (pp.c - pp.t) + j * pp.c;
+                int64_t q = j ? p - pp.c : r;
+                int64_t hi = std::min<int64_t>(p + pp.t, n - 1);
+                int64_t ce = std::min<int64_t>(hi + pp.c, n - 1);
+                int64_t m = hi - p + 1;
+                elems += (double)(m * ((hi - q + 1) + (ce - p + 1) - m));
+                flops += (double)(4 * m * (hi - q) + 4 * m * (ce - p) + 6 * m);
+                ++steps;
+            }
+        }
+    }
+    out->steps = steps;
+    out->critical_cycles = crit;
+    out->alg_elements = elems;
+    out->alg_bytes = 2.0 * (double)elem_size(dtype) * elems;
+    out->alg_flops = flops;
+    return BB_SUCCESS;
+}
+
+bb_status bb_launch_count(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const bb_config *cfg,
+                          int64_t *launches)
+{
+    if (!launches) return BB_ERR_INVALID_VALUE;
+    Plan P;
+    bb_status s = make_plan(n, b, dtype, batch, cfg, P);
+    if (s != BB_SUCCESS) return s;
+    if (n == 0 || batch == 0) {
+        *launches = 0;
+        return BB_SUCCESS;
+    }
+    int64_t L = 2; // pack + extract
+    for (const PassPlan &pp : P.passes)
+        L += (P.cfg.schedule == BB_SCHED_CYCLE) ? pp.cycles : (pp.nsweeps > 0 ? 1 : 0);
+    *launches = L;
+    return BB_SUCCESS;
+}
+
+const char *bb_status_string(bb_status s)
+{
+    switch (s) {
+    case BB_SUCCESS: return "BB_SUCCESS";
+    case BB_ERR_INVALID_VALUE: return "BB_ERR_INVALID_VALUE: invalid argument";
+    case BB_ERR_NOT_SUPPORTED: return "BB_ERR_NOT_SUPPORTED: unsupported dtype or configuration";
+    case BB_ERR_OUT_OF_MEMORY: return "BB_ERR_OUT_OF_MEMORY: device allocation failed";
+    case BB_ERR_CUDA: return "BB_ERR_CUDA: CUDA runtime or launch failure";
+    case BB_ERR_INTERNAL: return "BB_ERR_INTERNAL: internal invariant violated";
+    }
+    return "unknown bb_status";
+}
+
+int32_t bb_version(void) { return BB_VERSION; }
+
+} // extern "C"

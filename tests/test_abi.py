@@ -1,0 +1,126 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every
+symbol include/bandbidiag.h declares, validates arguments synchronously, and
+its host-side plan matches the oracle's independent enumeration exactly."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import oracle
+import paper_2510_12705_b200 as bb
+from paper_2510_12705_b200 import _native as N
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "bandbidiag.h")
+
+
+def _declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(bb_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = N.lib()
+    names = _declared()
+    assert len(names) >= 10
+    for name in names:
+        assert hasattr(L, name), name
+    assert sorted(N.EXPORTED) == names
+
+
+def test_version_and_status_strings():
+    assert bb.bb_version() == 100
+    for s in range(6):
+        assert N.status_string(s).startswith("BB_")
+
+
+def _raw(fn, *args):
+    return getattr(N.lib(), fn)(*args)
+
+
+def test_validation_is_synchronous_and_needs_no_device():
+    L = N.lib()
+    dummy = 0x1000
+    # n < 0, b < 0
+    assert L.bb_band_to_bidiag(-1, 4, N.BB_F64, dummy, 5, dummy, dummy, None) == N.BB_ERR_INVALID_VALUE
+    assert L.bb_band_to_bidiag(8, -1, N.BB_F64, dummy, 5, dummy, dummy, None) == N.BB_ERR_INVALID_VALUE
+    # ldband < b + 1
+    assert L.bb_band_to_bidiag(8, 4, N.BB_F64, dummy, 4, dummy, dummy, None) == N.BB_ERR_INVALID_VALUE
+    # null pointers with n > 0
+    assert L.bb_band_to_bidiag(8, 4, N.BB_F64, None, 5, dummy, dummy, None) == N.BB_ERR_INVALID_VALUE
+    assert L.bb_band_to_bidiag(8, 4, N.BB_F64, dummy, 5, None, dummy, None) == N.BB_ERR_INVALID_VALUE
+    # unknown dtype
+    assert L.bb_band_to_bidiag(8, 4, 7, dummy, 5, dummy, dummy, None) == N.BB_ERR_NOT_SUPPORTED
+    # n == 0 / batch == 0: no-op success, no device touched
+    assert L.bb_band_to_bidiag(0, 4, N.BB_F64, None, 5, None, None, None) == N.BB_SUCCESS
+    assert L.bb_band_to_bidiag_batched(8, 4, N.BB_F64, 0, None, 5, 40, None, 8, None, 7, None) == N.BB_SUCCESS
+    # overlapping batch strides
+    assert L.bb_band_to_bidiag_batched(8, 4, N.BB_F64, 2, dummy, 5, 39, dummy, 8, dummy, 7,
+                                       None) == N.BB_ERR_INVALID_VALUE
+    assert L.bb_band_to_bidiag_batched(8, 4, N.BB_F64, 2, dummy, 5, 40, dummy, 7, dummy, 7,
+                                       None) == N.BB_ERR_INVALID_VALUE
+    # negative tilewidth in the config; workspace too small
+    cfg = N.bb_config(-1, 0, 0, 0, 0, 0)
+    assert L.bb_band_to_bidiag_ex(8, 4, N.BB_F64, dummy, 5, dummy, dummy, ctypes.byref(cfg), dummy, 1 << 20,
+                                  None) == N.BB_ERR_INVALID_VALUE
+    cfg = N.bb_config(2, 0, 0, 0, 0, 0)
+    assert L.bb_band_to_bidiag_ex(8, 4, N.BB_F64, dummy, 5, dummy, dummy, ctypes.byref(cfg), dummy, 16,
+                                  None) == N.BB_ERR_INVALID_VALUE
+    # bad threads_per_block
+    cfg = N.bb_config(2, 33, 0, 0, 0, 0)
+    assert L.bb_band_to_bidiag_ex(8, 4, N.BB_F64, dummy, 5, dummy, dummy, ctypes.byref(cfg), dummy, 1 << 20,
+                                  None) == N.BB_ERR_INVALID_VALUE
+
+
+def test_window_too_large_is_not_supported():
+    # fp64, c = 512, t = 200: (t+1)(2c+t+1) * 8 B far above 227 KB of shared memory
+    with pytest.raises(N.BBError) as ei:
+        N.bb_workspace_size(4096, 512, N.BB_F64, 1, N.bb_config(200, 0, 0, 0, 0, 0))
+    assert ei.value.status == N.BB_ERR_NOT_SUPPORTED
+
+
+def test_no_cpu_fallback_without_device():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("device present")
+    # valid arguments but no GPU: the compute entry points fail loudly
+    L = N.lib()
+    buf = (ctypes.c_double * 64)()
+    s = L.bb_band_to_bidiag(8, 4, N.BB_F64, ctypes.addressof(buf), 5, ctypes.addressof(buf),
+                            ctypes.addressof(buf), None)
+    assert s in (N.BB_ERR_CUDA, N.BB_ERR_OUT_OF_MEMORY)
+
+
+@pytest.mark.parametrize("n,b,dt,tw,es", [
+    (64, 8, N.BB_F64, 4, 8), (1024, 32, N.BB_F64, 16, 8), (1024, 32, N.BB_F32, 32, 4),
+    (999, 37, N.BB_F16, 10, 2), (300, 299, N.BB_F64, 16, 8), (50, 60, N.BB_F32, 7, 4),
+])
+def test_plan_matches_oracle_enumeration(n, b, dt, tw, es):
+    st = N.bb_plan(n, b, dt, 1, N.bb_config(tw, 0, 0, 0, 0, 0))
+    w = oracle.workload(n, b, tw, es)
+    assert st["passes"] == w["passes"]
+    assert st["steps"] == w["steps"]
+    assert st["critical_cycles"] == w["critical_cycles"]
+    assert st["alg_elements"] == w["elements"]
+    assert st["alg_bytes"] == w["bytes"]
+    assert st["alg_flops"] == w["flops"]
+    beff = min(b, n - 1)
+    assert st["ldw"] == beff + 2 * st["tw"] + 1      # band + 2 tw headroom
+    assert st["ku"] == beff + st["tw"]
+
+
+def test_default_tilewidth_per_dtype():
+    # 16 for FP64, 32 for FP32 (one 128-byte line); fp16 uses 32
+    assert N.bb_plan(4096, 128, N.BB_F64)["tw"] == 16
+    assert N.bb_plan(4096, 128, N.BB_F32)["tw"] == 32
+    assert N.bb_plan(4096, 128, N.BB_F16)["tw"] == 32
+
+
+def test_launch_count():
+    # pack + one persistent launch per pass + extract
+    assert N.bb_launch_count(32768, 128, N.BB_F64) == 8 + 2
+    assert N.bb_launch_count(1024, 1, N.BB_F64) == 2
+    cyc = N.bb_launch_count(64, 8, N.BB_F64, 1, N.bb_config(4, 0, 0, 0, N.BB_SCHED_CYCLE, 0))
+    assert cyc == 2 + oracle.workload(64, 8, 4, 8)["critical_cycles"]

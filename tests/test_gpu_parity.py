@@ -1,0 +1,160 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs, element by element on |d|, |e| and on the singular
+values, within the north_star tolerances.  Structural
+zeros are checked exactly on the working band the kernels leave behind."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests.gpu_util import compare, gpu_reduce, tol
+
+pytestmark = pytest.mark.gpu
+
+
+def _bb():
+    import paper_2510_12705_b200 as bb
+    return bb
+
+
+# ------------------------------------------------ BASELINE config 1 (n=64, b=8, fp64)
+@pytest.mark.parametrize("tw", [1, 4, 7])
+@pytest.mark.parametrize("seed", range(3))
+@pytest.mark.parametrize("sched", ["flags", "cycle"])
+def test_config1_n64_b8_fp64(tw, seed, sched):
+    bb = _bb()
+    band = synth.random_band(64, 8, "f64", seed=seed)
+    cfg = bb.Config(tw=tw, schedule=bb.BB_SCHED_CYCLE if sched == "cycle" else bb.BB_SCHED_FLAGS)
+    d, e = gpu_reduce(band, 8, cfg=cfg)
+    compare(band, 8, tw, "f64", d, e)
+
+
+# ------------------------------------------------ BASELINE config 2 (n=1024, b=32)
+@pytest.mark.parametrize("dtype,tw", [("f64", 16), ("f32", 32), ("f64", 32), ("f32", 16)])
+def test_config2_n1024_b32(dtype, tw):
+    band = synth.random_band(1024, 32, dtype, seed=1)
+    d, e = gpu_reduce(band, 32, tw=tw)
+    compare(band, 32, tw, dtype, d, e)
+
+
+# ------------------------------------------------ config 3 shape, oracle-sized
+@pytest.mark.parametrize("dtype", ["f16", "f32", "f64"])
+@pytest.mark.parametrize("tw", [8, 16, 32, 63])
+def test_config3_shape_precision_tilewidth(dtype, tw):
+    n, b = 1537, 64   # ragged: not a multiple of any tile
+    band = synth.random_band(n, b, dtype, seed=2)
+    d, e = gpu_reduce(band, b, tw=tw)
+    compare(band, b, tw, dtype, d, e, svals=(dtype != "f16"))
+
+
+@pytest.mark.parametrize("threads,maxb", [(64, 1), (128, 2), (256, 0), (512, 8)])
+def test_launch_configs_bitwise_identical(threads, maxb):
+    # the flag schedule orders every conflicting pair, so the result does not
+    # depend on the launch configuration
+    bb = _bb()
+    band = synth.random_band(700, 40, "f64", seed=3)
+    ref = gpu_reduce(band, 40, tw=16)
+    got = gpu_reduce(band, 40, cfg=bb.Config(tw=16, threads_per_block=threads, max_blocks_per_sm=maxb))
+    assert np.array_equal(ref[0], got[0]) and np.array_equal(ref[1], got[1])
+
+
+@pytest.mark.parametrize("dtype", ["f16", "f32", "f64"])
+def test_flags_schedule_bitwise_equals_cycle_schedule(dtype):
+    bb = _bb()
+    band = synth.random_band(300, 24, dtype, seed=4)
+    a = gpu_reduce(band, 24, cfg=bb.Config(tw=8, schedule=bb.BB_SCHED_FLAGS))
+    c = gpu_reduce(band, 24, cfg=bb.Config(tw=8, schedule=bb.BB_SCHED_CYCLE))
+    assert np.array_equal(a[0], c[0]) and np.array_equal(a[1], c[1])
+
+
+def test_run_to_run_deterministic():
+    band = synth.random_band(2000, 48, "f32", seed=5)
+    a = gpu_reduce(band, 48, tw=32)
+    b2 = gpu_reduce(band, 48, tw=32)
+    assert np.array_equal(a[0], b2[0]) and np.array_equal(a[1], b2[1])
+
+
+# ------------------------------------------------ structural zeros, exact
+@pytest.mark.parametrize("dtype,tw", [("f64", 16), ("f32", 32), ("f16", 32)])
+def test_structural_zeros_exact(dtype, tw):
+    import torch
+    bb = _bb()
+    n, b = 900, 48
+    band = synth.random_band(n, b, dtype, seed=6)
+    ws = bb.Workspace(n, b, dtype, 1, tw=tw)
+    t = torch.from_numpy(band).cuda()
+    d, e = bb.band_to_bidiag(t, b, workspace=ws)
+    torch.cuda.synchronize()
+    W = ws.band_view()[0].double().cpu().numpy()       # (n, ldw): W[j, ku + i - j] = A(i, j)
+    ku = ws.stats["ku"]
+    mask = np.ones_like(W, dtype=bool)
+    mask[:, ku] = False                 # diagonal i = j
+    mask[1:, ku - 1] = False            # superdiagonal i = j - 1
+    assert np.count_nonzero(W[mask]) == 0
+    assert np.array_equal(W[:, ku], d.double().cpu().numpy())
+
+
+# ------------------------------------------------ edge cases
+@pytest.mark.parametrize("n,b,tw", [(1, 0, 4), (1, 5, 4), (2, 1, 4), (2, 7, 4), (3, 2, 1), (3, 9, 2), (5, 4, 3),
+                                    (17, 16, 16), (33, 2, 5), (40, 39, 38), (100, 0, 3), (100, 1, 3),
+                                    (129, 128, 16), (130, 3, 2)])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_edge_shapes(n, b, tw, dtype):
+    band = synth.random_band(n, b, dtype, seed=7)
+    d, e = gpu_reduce(band, b, tw=tw)
+    if min(b, n - 1) <= 1:
+        # already bidiagonal: copied through bit-exactly
+        assert np.array_equal(d, band[:, b])
+        if n > 1 and b >= 1:
+            assert np.array_equal(e, band[1:, b - 1])
+        elif n > 1:
+            assert np.all(e == 0)
+    compare(band, b, tw, dtype, d, e)
+
+
+def test_empty_matrix():
+    import torch
+    bb = _bb()
+    d, e = bb.band_to_bidiag(torch.zeros(0, 5, dtype=torch.float64, device="cuda"), 4)
+    assert d.numel() == 0 and e.numel() == 0
+
+
+def test_ldband_padding_and_nonneg():
+    bb = _bb()
+    n, b = 400, 20
+    band = synth.random_band(n, b, "f64", seed=8, ldband=b + 7)
+    d, e = gpu_reduce(band, b, cfg=bb.Config(tw=8, nonneg=True))
+    assert np.all(d >= 0) and np.all(e >= 0)
+    compare(band, b, 8, "f64", d, e)
+
+
+def test_batched_matches_single():
+    n, b, B = 500, 32, 5
+    bands = synth.random_band_batch(B, n, b, "f64", seed=9)
+    d, e = gpu_reduce(bands, b, tw=16, batched=True)
+    for k in range(B):
+        ds, es = gpu_reduce(bands[k], b, tw=16)
+        assert np.array_equal(d[k], ds) and np.array_equal(e[k], es)
+        compare(bands[k], b, 16, "f64", d[k], e[k], svals=False)
+
+
+def test_host_entry_point_matches_device():
+    bb = _bb()
+    band = synth.random_band(600, 30, "f32", seed=10)
+    dh, eh = bb.band_to_bidiag_host(band, 30, tw=16)
+    dd, ed = gpu_reduce(band, 30, tw=16)
+    assert np.array_equal(dh.numpy(), dd) and np.array_equal(eh.numpy(), ed)
+
+
+# ------------------------------------------------ known-spectrum accuracy
+@pytest.mark.parametrize("dtype,bound", [("f64", 1e-11), ("f32", 1e-4), ("f16", 5e-2)])
+@pytest.mark.parametrize("kind", ["arith", "log", "qcirc"])
+def test_known_spectrum_accuracy(dtype, bound, kind):
+    from tests.lapack_ref import bidiag_svals
+    n, b = 256, 8
+    sig = synth.spectrum(kind, n)
+    Ab = synth.dense_to_upper_band(synth.known_spectrum_dense(n, sig, seed=3), b)
+    band = synth.dense_to_band(Ab, b, dtype)
+    d, e = gpu_reduce(band, b, tw=4)
+    s = bidiag_svals(d.astype(np.float64), e.astype(np.float64))
+    assert np.max(np.abs(s - np.sort(sig)[::-1])) / np.max(sig) < bound
