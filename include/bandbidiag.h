@@ -92,7 +92,10 @@ typedef enum {
                          /* Slow (about s*n launches per pass); reference/debug.    */
 
 /* bb_config.flags */
-#define BB_FLAG_NONNEG_OUTPUT 0x1u /* return |d|, |e| */
+#define BB_FLAG_NONNEG_OUTPUT 0x1u /* return |d|, |e|                                    */
+#define BB_FLAG_GENERIC_KERNEL 0x2u /* force the generic shared-memory step kernel (the   */
+                                   /* register kernel serves tw <= 32); results are      */
+                                   /* bitwise identical, for testing                     */
 
 /* Tuning knobs, the paper's hyperparameter triple.
  * Zero-initialise for defaults. */
@@ -104,6 +107,14 @@ typedef struct {
                                /* values below auto are raised to auto                  */
     int32_t schedule;          /* BB_SCHED_*                                            */
     uint32_t flags;            /* BB_FLAG_*                                             */
+    /* Optional timing hooks (NULL/0 = off): an array of cudaEvent_t (as void*),
+     * at least passes + 3 long, recorded on `stream`: [0] before the pack
+     * kernel, [1] after it, [1 + p] after pass p (p = 1..passes), [passes + 2]
+     * after the extract kernel.  Used by bench.py to time the pass kernels
+     * with CUDA events on the launching stream.  Too short an array is
+     * BB_ERR_INVALID_VALUE. */
+    void **timing_events;
+    int32_t num_timing_events;
 } bb_config;
 
 /* Plan of one call (host-only arithmetic, no device work). */

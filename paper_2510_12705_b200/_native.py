@@ -22,6 +22,7 @@ BB_ERR_CUDA = 4
 BB_ERR_INTERNAL = 5
 BB_SCHED_AUTO, BB_SCHED_FLAGS, BB_SCHED_CYCLE = 0, 1, 2
 BB_FLAG_NONNEG_OUTPUT = 0x1
+BB_FLAG_GENERIC_KERNEL = 0x2
 
 EXPORTED = [
     "bb_band_to_bidiag", "bb_band_to_bidiag_batched", "bb_band_to_bidiag_ex",
@@ -33,7 +34,8 @@ EXPORTED = [
 class bb_config(ctypes.Structure):
     _fields_ = [("tw", ctypes.c_int32), ("threads_per_block", ctypes.c_int32),
                 ("max_blocks_per_sm", ctypes.c_int32), ("dep_distance", ctypes.c_int32),
-                ("schedule", ctypes.c_int32), ("flags", ctypes.c_uint32)]
+                ("schedule", ctypes.c_int32), ("flags", ctypes.c_uint32),
+                ("timing_events", ctypes.POINTER(ctypes.c_void_p)), ("num_timing_events", ctypes.c_int32)]
 
 
 class bb_plan_stats(ctypes.Structure):

@@ -6,6 +6,7 @@ Every step of the reduction runs in the CUDA kernels behind
 """
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import torch
@@ -35,10 +36,22 @@ class Config:
     dep_distance: int = 0
     schedule: int = N.BB_SCHED_AUTO
     nonneg: bool = False
+    generic: bool = False       # force the generic shared-memory step kernel (testing)
+    timing_events: tuple = ()   # torch.cuda.Event objects (enable_timing=True), >= passes + 3
 
     def c(self) -> N.bb_config:
-        return N.bb_config(self.tw, self.threads_per_block, self.max_blocks_per_sm, self.dep_distance,
-                           self.schedule, N.BB_FLAG_NONNEG_OUTPUT if self.nonneg else 0)
+        flags = (N.BB_FLAG_NONNEG_OUTPUT if self.nonneg else 0) | (N.BB_FLAG_GENERIC_KERNEL if self.generic else 0)
+        cfg = N.bb_config(self.tw, self.threads_per_block, self.max_blocks_per_sm, self.dep_distance,
+                          self.schedule, flags)
+        if self.timing_events:
+            for ev in self.timing_events:
+                if ev.cuda_event == 0:      # torch creates events lazily
+                    ev.record()
+            arr = (ctypes.c_void_p * len(self.timing_events))(*[ev.cuda_event for ev in self.timing_events])
+            cfg.timing_events = arr
+            cfg.num_timing_events = len(self.timing_events)
+            cfg._keep = arr
+        return cfg
 
 
 def _stream() -> int:

@@ -6,9 +6,11 @@
 // bb_kernels.cuh.  No CPU fallback exists: without a usable CUDA device every
 // compute entry point returns BB_ERR_CUDA.
 #include "bb_kernels.cuh"
+#include "bb_pass_v2.cuh"
 #include "bandbidiag.h"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -40,6 +42,10 @@ struct PassPlan {
     int LT, LW;
     size_t smem;     // dynamic shared memory bytes
     int threads;
+    // register kernel (bb_pass_v2.cuh)
+    bool v2 = false;
+    int mt = 0, ntc = 0, a0 = 0, b0 = 0, LW2 = 0;
+    size_t smem2 = 0;
 };
 
 struct Plan {
@@ -74,6 +80,7 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
         return BB_ERR_INVALID_VALUE;
     if (cfg.threads_per_block && (cfg.threads_per_block % 32 || cfg.threads_per_block > 512))
         return BB_ERR_INVALID_VALUE;
+    if (cfg.num_timing_events < 0) return BB_ERR_INVALID_VALUE;
     if (cfg.schedule == BB_SCHED_AUTO) cfg.schedule = BB_SCHED_FLAGS;
     P.n = n;
     P.batch = batch;
@@ -108,10 +115,22 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
             int thr = cfg.threads_per_block;
             if (!thr) thr = (int)std::min<int64_t>(256, std::max<int64_t>(64, (c + t + 31) / 32 * 32));
             pp.threads = thr;
+            // register kernel: reflector length t+1 <= 33, c + t + 1 + 64 <= 1024 threads
+            const int tb = (int)(c - t);
+            pp.a0 = tb >= 4 ? 2 : (tb >= 2 ? 4 : 6);
+            pp.b0 = tb >= 4 ? 3 : pp.a0;
+            if (pp.s > (tb == 1 ? 3 : 2)) pp.a0 = pp.b0 = 2 * pp.s; // user asked for a larger distance
+            pp.mt = t + 1 <= 9 ? 9 : (t + 1 <= 17 ? 17 : (t + 1 <= 33 ? 33 : 0));
+            pp.ntc = (int)((c + t + 1 + 31) / 32 * 32);
+            pp.LW2 = round_odd(pp.mt);
+            pp.smem2 = cs * (size_t)(2 * pp.mt + 4 + (size_t)pp.LW2 * (c + t + 1)) + 16;
+            pp.v2 = pp.mt > 0 && pp.ntc + 64 <= 512 && !(cfg.flags & BB_FLAG_GENERIC_KERNEL) &&
+                    pp.smem2 <= (size_t)kSmemOptinFallback;
             P.passes.push_back(pp);
             c -= t;
         }
     }
+    if (cfg.timing_events && cfg.num_timing_events < (int)P.passes.size() + 3) return BB_ERR_INVALID_VALUE;
     P.cfg = cfg;
     size_t es = elem_size(dtype);
     P.band_bytes = align_up((size_t)batch * (size_t)n * (size_t)P.ldw * es);
@@ -166,9 +185,12 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
     const int n = (int)P.n;
     const int batch = (int)P.batch;
 
+    cudaEvent_t *ev = reinterpret_cast<cudaEvent_t *>(P.cfg.timing_events);
+    auto mark = [&](int k) { if (ev) cudaEventRecord(ev[k], st); };
     if (!P.passes.empty()) {
         if (cudaMemsetAsync(flags, 0, P.flag_bytes + P.counter_bytes, st) != cudaSuccess) return BB_ERR_CUDA;
     }
+    mark(0);
     {
         int64_t total = (int64_t)batch * mat_stride;
         int thr = 256;
@@ -177,6 +199,7 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
             reinterpret_cast<const S *>(band), ldband, stride_band, (int)b_in, (int)P.b_eff, W, mat_stride,
             (int)P.ldw, (int)P.ku, n, batch);
     }
+    mark(1);
     for (size_t pi = 0; pi < P.passes.size(); ++pi) {
         const PassPlan &pp = P.passes[pi];
         if ((int)pp.smem > di.smem_optin) return BB_ERR_NOT_SUPPORTED;
@@ -207,6 +230,67 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
                 dim3 grid((unsigned)std::max(rmax, 1), (unsigned)batch);
                 kern<<<grid, pp.threads, pp.smem, st>>>(a);
             }
+        } else if (pp.v2) {
+            bb::PassArgsV2 a2{};
+            a2.W = W;
+            a2.mat_stride = mat_stride;
+            a2.ldw = (int)P.ldw;
+            a2.ku = (int)P.ku;
+            a2.n = n;
+            a2.c = pp.c;
+            a2.t = pp.t;
+            a2.a0 = pp.a0;
+            a2.b0 = pp.b0;
+            a2.batch = batch;
+            a2.nsweeps = pp.nsweeps;
+            a2.progress = a.progress;
+            a2.counter = a.counter;
+            a2.ntc = pp.ntc;
+            a2.LW = pp.LW2;
+            void (*kern)(bb::PassArgsV2) = nullptr;
+            const int nt = pp.ntc + 64;
+            if (nt <= 256) {
+                kern = pp.mt == 9 ? bb::pass_v2_kernel<S, 9, 256>
+                                  : (pp.mt == 17 ? bb::pass_v2_kernel<S, 17, 256> : bb::pass_v2_kernel<S, 33, 256>);
+            } else {
+                kern = pp.mt == 9 ? bb::pass_v2_kernel<S, 9, 512>
+                                  : (pp.mt == 17 ? bb::pass_v2_kernel<S, 17, 512> : bb::pass_v2_kernel<S, 33, 512>);
+            }
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem2) != cudaSuccess)
+                return BB_ERR_CUDA;
+            int occ = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, pp.smem2) != cudaSuccess)
+                return BB_ERR_CUDA;
+            if (P.cfg.max_blocks_per_sm > 0) occ = std::min(occ, (int)P.cfg.max_blocks_per_sm);
+            occ = std::max(occ, 1);
+            int64_t tasks = (int64_t)pp.nsweeps * batch;
+            int64_t grid = std::min<int64_t>(tasks, (int64_t)occ * di.sms);
+            const char *tf = getenv("BB_TRACE_FILE");
+            const char *tp = getenv("BB_TRACE_PASS");
+            unsigned long long *tbuf = nullptr;
+            if (tf && (int)pi == (tp ? atoi(tp) : 0)) {
+                a2.trace_sweeps = std::min(pp.nsweeps, 1024);
+                a2.trace_steps = (int)sweep_len_h(n, pp.c, pp.t, 0);
+                size_t tb = (size_t)a2.trace_sweeps * a2.trace_steps * 16 * sizeof(unsigned long long);
+                if (cudaMalloc(&tbuf, tb) == cudaSuccess) {
+                    cudaMemsetAsync(tbuf, 0, tb, st);
+                    a2.trace = tbuf;
+                }
+            }
+            if (grid >= 1) kern<<<(unsigned)grid, nt, pp.smem2, st>>>(a2);
+            if (tbuf) {
+                size_t cnt = (size_t)a2.trace_sweeps * a2.trace_steps * 16;
+                std::vector<unsigned long long> h(cnt);
+                cudaMemcpyAsync(h.data(), tbuf, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                if (FILE *f = fopen(tf, "wb")) {
+                    int hdr[6] = {a2.trace_sweeps, a2.trace_steps, pp.c, pp.t, pp.s, (int)grid};
+                    fwrite(hdr, sizeof(int), 6, f);
+                    fwrite(h.data(), sizeof(unsigned long long), cnt, f);
+                    fclose(f);
+                }
+                cudaFree(tbuf);
+            }
         } else {
             auto kern = bb::pass_flags_kernel<S>;
             if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem) != cudaSuccess)
@@ -218,10 +302,37 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
             occ = std::max(occ, 1);
             int64_t tasks = (int64_t)pp.nsweeps * batch;
             int64_t grid = std::min<int64_t>(tasks, (int64_t)occ * di.sms);
-            if (grid < 1) continue;
-            kern<<<(unsigned)grid, pp.threads, pp.smem, st>>>(a);
+            // debug tracing (BB_TRACE_FILE, BB_TRACE_PASS): per-step timestamps of
+            // matrix 0's first sweeps in one pass, dumped after that pass
+            const char *tf = getenv("BB_TRACE_FILE");
+            const char *tp = getenv("BB_TRACE_PASS");
+            unsigned long long *tbuf = nullptr;
+            if (tf && (int)pi == (tp ? atoi(tp) : 0)) {
+                a.trace_sweeps = std::min(pp.nsweeps, 1024);
+                a.trace_steps = (int)sweep_len_h(n, pp.c, pp.t, 0);
+                size_t tb = (size_t)a.trace_sweeps * a.trace_steps * 4 * sizeof(unsigned long long);
+                if (cudaMalloc(&tbuf, tb) == cudaSuccess) {
+                    cudaMemsetAsync(tbuf, 0, tb, st);
+                    a.trace = tbuf;
+                }
+            }
+            if (grid >= 1) kern<<<(unsigned)grid, pp.threads, pp.smem, st>>>(a);
+            if (tbuf) {
+                size_t cnt = (size_t)a.trace_sweeps * a.trace_steps * 4;
+                std::vector<unsigned long long> h(cnt);
+                cudaMemcpyAsync(h.data(), tbuf, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                if (FILE *f = fopen(tf, "wb")) {
+                    int hdr[6] = {a.trace_sweeps, a.trace_steps, pp.c, pp.t, pp.s, (int)grid};
+                    fwrite(hdr, sizeof(int), 6, f);
+                    fwrite(h.data(), sizeof(unsigned long long), cnt, f);
+                    fclose(f);
+                }
+                cudaFree(tbuf);
+            }
         }
         if (cudaGetLastError() != cudaSuccess) return BB_ERR_CUDA;
+        mark(2 + (int)pi);
     }
     {
         int64_t total = (int64_t)batch * n;
@@ -231,6 +342,7 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
             W, mat_stride, (int)P.ldw, (int)P.ku, n, batch, reinterpret_cast<S *>(d_out), stride_d,
             reinterpret_cast<S *>(e_out), stride_e, (P.cfg.flags & BB_FLAG_NONNEG_OUTPUT) ? 1 : 0);
     }
+    mark(2 + (int)P.passes.size());
     if (cudaGetLastError() != cudaSuccess) return BB_ERR_CUDA;
     return BB_SUCCESS;
 }

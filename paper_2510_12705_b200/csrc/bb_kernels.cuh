@@ -51,6 +51,22 @@ __device__ __forceinline__ int ld_acquire(const int *p)
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ int ld_relaxed(const int *p)
+{
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// spin until *p >= need: relaxed polling, one acquire fence on success
+__device__ __forceinline__ void wait_geq(const int *p, int need)
+{
+    if (ld_relaxed(p) < need) {
+        while (ld_relaxed(p) < need) {
+        }
+    }
+    fence_acq_rel();
+}
 __device__ __forceinline__ void st_release(int *p, int v)
 {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -127,6 +143,66 @@ __device__ __forceinline__ void house_warp(const C *x, int stride, int m, C *v, 
     for (int k = lane; k < m; k += 32) v[k] = (k == 0) ? C(1) : x[k * stride] / den;
 }
 
+// Copy `ncols` columns of `rows` elements from global (column k at g + k*gstride)
+// into shared memory (column k at s + k*sstride) with every thread of the CTA.
+// U loads per thread are issued back to back before their shared-memory
+// stores, so a step's window arrives in ~1 L2 round trip, not one per column.
+template <class S, class C, int U>
+__device__ __forceinline__ void gather_cols(const S *__restrict__ g, int64_t gstride, int rows, int ncols,
+                                            C *__restrict__ s, int sstride)
+{
+    const int total = rows * ncols;
+    if (total <= 0) return;
+    const int nthr = blockDim.x;
+    int e = threadIdx.x;
+    int k = e / rows, ii = e - k * rows;
+    const int dk = nthr / rows, dii = nthr - dk * rows;
+    while (e < total) {
+        C buf[U];
+        int so[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            so[u] = -1;
+            if (e < total) {
+                buf[u] = ldg_cg(g + k * gstride + ii);
+                so[u] = ii + k * sstride;
+            }
+            e += nthr;
+            ii += dii;
+            k += dk;
+            if (ii >= rows) { ii -= rows; ++k; }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (so[u] >= 0) s[so[u]] = buf[u];
+    }
+}
+
+template <class S, class C>
+__device__ __forceinline__ void scatter_cols(S *__restrict__ g, int64_t gstride, int rows, int ncols,
+                                             const C *__restrict__ s, int sstride)
+{
+    const int total = rows * ncols;
+    if (total <= 0) return;
+    const int nthr = blockDim.x;
+    int e = threadIdx.x;
+    int k = e / rows, ii = e - k * rows;
+    const int dk = nthr / rows, dii = nthr - dk * rows;
+    for (; e < total; e += nthr) {
+        stg(g + k * gstride + ii, s[ii + k * sstride]);
+        ii += dii;
+        k += dk;
+        if (ii >= rows) { ii -= rows; ++k; }
+    }
+}
+
+__device__ __forceinline__ unsigned long long gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 struct PassArgs {
     void *W;            // working bands (batch of them)
     int64_t mat_stride; // elements between matrices
@@ -138,7 +214,16 @@ struct PassArgs {
     int *counter;       // next task to claim (this pass)
     int LT, LW;         // shared-memory leading dimensions (odd)
     int cycle_T;        // BB_SCHED_CYCLE: the cycle this launch runs
+    unsigned long long *trace; // debug: per-step timestamps (nullptr = off)
+    int trace_sweeps, trace_steps;
 };
+
+// debug tracing: timestamps [wait start, wait end, window staged, stored+released]
+#define TRACE_MARK(slot)                                                                         \
+    do {                                                                                         \
+        if (a.trace && threadIdx.x == 0 && mat == 0 && r < a.trace_sweeps && j < a.trace_steps) \
+            a.trace[((int64_t)r * a.trace_steps + j) * 4 + (slot)] = gtimer();                  \
+    } while (0)
 
 __device__ __forceinline__ int sweep_len(int n, int c, int t, int r)
 {
@@ -172,16 +257,11 @@ __device__ void bulge_step(const PassArgs &a, int mat, int r, int j, typename Co
     const int64_t ldw = a.ldw;
 
     // ---- stage the window: tall columns p..hi (rows q..hi), wide hi+1..ce (rows p..hi)
-    for (int k = warp; k < m; k += nwarps) {
-        const S *col = W + (ku + q - (p + k)) + (int64_t)(p + k) * ldw;
-        for (int ii = lane; ii < rowsT; ii += 32) T[ii + k * LT] = ldg_cg(col + ii);
-    }
-    for (int k = warp; k < nW; k += nwarps) {
-        const int jc = hi + 1 + k;
-        const S *col = W + (ku + p - jc) + (int64_t)jc * ldw;
-        for (int kk = lane; kk < m; kk += 32) R[kk + k * LW] = ldg_cg(col + kk);
-    }
+    // Column k of either part starts (ldw - 1) elements after column k-1.
+    gather_cols<S, C, 8>(W + (ku + q - p) + (int64_t)p * ldw, ldw - 1, rowsT, m, T, LT);
+    gather_cols<S, C, 8>(W + (ku + p - (hi + 1)) + (int64_t)(hi + 1) * ldw, ldw - 1, m, nW, R, LW);
     __syncthreads();
+    TRACE_MARK(2);
 
     // ---- row reflector from A[q, p..hi] (Alg. 2 lines 3-6)
     if (warp == 0) {
@@ -234,15 +314,8 @@ __device__ void bulge_step(const PassArgs &a, int mat, int r, int j, typename Co
     __syncthreads();
 
     // ---- write the window back
-    for (int k = warp; k < m; k += nwarps) {
-        S *col = W + (ku + q - (p + k)) + (int64_t)(p + k) * ldw;
-        for (int ii = lane; ii < rowsT; ii += 32) stg(col + ii, T[ii + k * LT]);
-    }
-    for (int k = warp; k < nW; k += nwarps) {
-        const int jc = hi + 1 + k;
-        S *col = W + (ku + p - jc) + (int64_t)jc * ldw;
-        for (int kk = lane; kk < m; kk += 32) stg(col + kk, R[kk + k * LW]);
-    }
+    scatter_cols<S, C>(W + (ku + q - p) + (int64_t)p * ldw, ldw - 1, rowsT, m, T, LT);
+    scatter_cols<S, C>(W + (ku + p - (hi + 1)) + (int64_t)(hi + 1) * ldw, ldw - 1, m, nW, R, LW);
 }
 
 // ---- BB_SCHED_FLAGS: one persistent launch per pass ----------------------
@@ -271,6 +344,7 @@ __global__ void __launch_bounds__(512) pass_flags_kernel(PassArgs a)
         const int Jp = r > 0 ? sweep_len(a.n, a.c, a.t, r - 1) : 0;
         int *prog = a.progress + (int64_t)mat * a.n;
         for (int j = 0; j < J; ++j) {
+            TRACE_MARK(0);
             if (r > 0) {
                 if (threadIdx.x == 0) {
                     const int need = min(j + a.s, Jp);
@@ -279,12 +353,14 @@ __global__ void __launch_bounds__(512) pass_flags_kernel(PassArgs a)
                 }
                 __syncthreads();
             }
+            TRACE_MARK(1);
             bulge_step<S>(a, mat, r, j, sm);
             __syncthreads();
             if (threadIdx.x == 0) {
                 __threadfence();
                 st_release(prog + r, j + 1);
             }
+            TRACE_MARK(3);
         }
     }
 }

@@ -53,8 +53,9 @@ def test_launch_configs_bitwise_identical(threads, maxb):
     # depend on the launch configuration
     bb = _bb()
     band = synth.random_band(700, 40, "f64", seed=3)
-    ref = gpu_reduce(band, 40, tw=16)
-    got = gpu_reduce(band, 40, cfg=bb.Config(tw=16, threads_per_block=threads, max_blocks_per_sm=maxb))
+    ref = gpu_reduce(band, 40, cfg=bb.Config(tw=16, generic=True))
+    got = gpu_reduce(band, 40, cfg=bb.Config(tw=16, threads_per_block=threads, max_blocks_per_sm=maxb,
+                                              generic=True))
     assert np.array_equal(ref[0], got[0]) and np.array_equal(ref[1], got[1])
 
 
@@ -62,9 +63,32 @@ def test_launch_configs_bitwise_identical(threads, maxb):
 def test_flags_schedule_bitwise_equals_cycle_schedule(dtype):
     bb = _bb()
     band = synth.random_band(300, 24, dtype, seed=4)
-    a = gpu_reduce(band, 24, cfg=bb.Config(tw=8, schedule=bb.BB_SCHED_FLAGS))
+    # same step arithmetic (generic kernel) under both schedules
+    a = gpu_reduce(band, 24, cfg=bb.Config(tw=8, schedule=bb.BB_SCHED_FLAGS, generic=True))
     c = gpu_reduce(band, 24, cfg=bb.Config(tw=8, schedule=bb.BB_SCHED_CYCLE))
     assert np.array_equal(a[0], c[0]) and np.array_equal(a[1], c[1])
+
+
+@pytest.mark.parametrize("dtype,tw", [("f64", 16), ("f32", 32), ("f16", 8), ("f64", 4)])
+def test_register_kernel_vs_generic_kernel(dtype, tw):
+    # two different step kernels (register-resident rows vs shared-memory
+    # window) agree with each other and with the oracle
+    bb = _bb()
+    n, b = 1100, 64
+    band = synth.random_band(n, b, dtype, seed=12)
+    d1, e1 = gpu_reduce(band, b, cfg=bb.Config(tw=tw))
+    d2, e2 = gpu_reduce(band, b, cfg=bb.Config(tw=tw, generic=True))
+    compare(band, b, tw, dtype, d1, e1, svals=False)
+    compare(band, b, tw, dtype, d2, e2, svals=False)
+
+
+@pytest.mark.parametrize("maxb", [1, 2, 3])
+def test_register_kernel_occupancy_bitwise_identical(maxb):
+    bb = _bb()
+    band = synth.random_band(3000, 96, "f64", seed=13)
+    ref = gpu_reduce(band, 96, tw=16)
+    got = gpu_reduce(band, 96, cfg=bb.Config(tw=16, max_blocks_per_sm=maxb))
+    assert np.array_equal(ref[0], got[0]) and np.array_equal(ref[1], got[1])
 
 
 def test_run_to_run_deterministic():
