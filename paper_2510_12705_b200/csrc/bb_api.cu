@@ -7,6 +7,7 @@
 // compute entry point returns BB_ERR_CUDA.
 #include "bb_kernels.cuh"
 #include "bb_pass_v2.cuh"
+#include "bb_pass_v3.cuh"
 #include "bandbidiag.h"
 
 #include <algorithm>
@@ -46,6 +47,9 @@ struct PassPlan {
     bool v2 = false;
     int mt = 0, ntc = 0, a0 = 0, b0 = 0, LW2 = 0;
     size_t smem2 = 0;
+    // multi-sweep kernel (bb_pass_v3.cuh)
+    int g3 = 0, ntg = 0, LDT3 = 0, LDW3 = 0, NS3 = 0;
+    size_t smem3 = 0;
 };
 
 struct Plan {
@@ -126,6 +130,25 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
             pp.smem2 = cs * (size_t)(2 * pp.mt + 4 + (size_t)pp.LW2 * (c + t + 1)) + 16;
             pp.v2 = pp.mt > 0 && pp.ntc + 64 <= 512 && !(cfg.flags & BB_FLAG_GENERIC_KERNEL) &&
                     pp.smem2 <= (size_t)kSmemOptinFallback;
+            // multi-sweep CTA (bb_pass_v3.cuh): G warp-groups of ntg threads (+ a release
+            // warp), NS = G + 2 window slots; needs target bandwidth >= max(4, G + 2)
+            pp.ntg = (int)((c + t + 31) / 32 * 32);
+            {
+                int G = pp.ntg <= 160 ? 3 : (pp.ntg <= 320 ? 2 : 0);
+                if (const char *e = getenv("BB_V3_G")) G = std::min(G, atoi(e));
+                if (!pp.v2) G = 0;
+                for (; G > 0; --G) {
+                    if (c - t < std::max(4, G + 2)) continue;
+                    const int WT = (int)t + G;
+                    pp.LDT3 = round_odd((int)c + G);
+                    pp.LDW3 = round_odd(WT);
+                    pp.NS3 = G + 2;
+                    size_t slot = (size_t)pp.LDT3 * WT + (size_t)pp.LDW3 * c;
+                    pp.smem3 = cs * (slot * pp.NS3 + (size_t)G * (2 * pp.mt + 4)) + 16;
+                    if (pp.smem3 <= (size_t)kSmemOptinFallback) break;
+                }
+                pp.g3 = G;
+            }
             P.passes.push_back(pp);
             c -= t;
         }
@@ -229,6 +252,72 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
                 int rmax = std::min(T / pp.s + 1, pp.nsweeps);
                 dim3 grid((unsigned)std::max(rmax, 1), (unsigned)batch);
                 kern<<<grid, pp.threads, pp.smem, st>>>(a);
+            }
+        } else if (pp.g3 > 0) {
+            const int G = pp.g3;
+            bb::PassArgsV3 a3{};
+            a3.W = W;
+            a3.mat_stride = mat_stride;
+            a3.ldw = (int)P.ldw;
+            a3.ku = (int)P.ku;
+            a3.n = n;
+            a3.c = pp.c;
+            a3.t = pp.t;
+            a3.a0 = pp.a0;
+            a3.b0 = pp.b0;
+            a3.batch = batch;
+            a3.nsweeps = pp.nsweeps;
+            a3.ngroups = (pp.nsweeps + G - 1) / G;
+            a3.progress = a.progress;
+            a3.counter = a.counter;
+            a3.ntg = pp.ntg;
+            a3.LDT = pp.LDT3;
+            a3.LDW = pp.LDW3;
+            a3.NS = pp.NS3;
+            if (const char *e = getenv("BB_V3_DBG")) a3.dbg = atoi(e);
+            const int nt = G * pp.ntg + 32;
+            void (*kern)(bb::PassArgsV3) = nullptr;
+#define BB_PICK3(GG, NTM)                                                                                          \
+    kern = pp.mt == 9 ? bb::pass_v3_kernel<S, 9, GG, NTM>                                                         \
+                      : (pp.mt == 17 ? bb::pass_v3_kernel<S, 17, GG, NTM> : bb::pass_v3_kernel<S, 33, GG, NTM>)
+            if (G == 3) { BB_PICK3(3, 512); }
+            else if (G == 2) { BB_PICK3(2, 672); }
+            else { BB_PICK3(1, 352); }
+#undef BB_PICK3
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem3) != cudaSuccess)
+                return BB_ERR_CUDA;
+            int occ = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, pp.smem3) != cudaSuccess)
+                return BB_ERR_CUDA;
+            if (P.cfg.max_blocks_per_sm > 0) occ = std::min(occ, (int)P.cfg.max_blocks_per_sm);
+            occ = std::max(occ, 1);
+            int64_t tasks = (int64_t)a3.ngroups * batch;
+            int64_t grid = std::min<int64_t>(tasks, (int64_t)occ * di.sms);
+            const char *tf = getenv("BB_TRACE_FILE");
+            const char *tp = getenv("BB_TRACE_PASS");
+            unsigned long long *tbuf = nullptr;
+            if (tf && (int)pi == (tp ? atoi(tp) : 0)) {
+                a3.trace_sweeps = std::min(pp.nsweeps, 1024);
+                a3.trace_steps = (int)sweep_len_h(n, pp.c, pp.t, 0);
+                size_t tb = (size_t)a3.trace_sweeps * a3.trace_steps * 16 * sizeof(unsigned long long);
+                if (cudaMalloc(&tbuf, tb) == cudaSuccess) {
+                    cudaMemsetAsync(tbuf, 0, tb, st);
+                    a3.trace = tbuf;
+                }
+            }
+            if (grid >= 1) kern<<<(unsigned)grid, nt, pp.smem3, st>>>(a3);
+            if (tbuf) {
+                size_t cnt = (size_t)a3.trace_sweeps * a3.trace_steps * 16;
+                std::vector<unsigned long long> h(cnt);
+                cudaMemcpyAsync(h.data(), tbuf, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                if (FILE *f = fopen(tf, "wb")) {
+                    int hdr[6] = {a3.trace_sweeps, a3.trace_steps, pp.c, pp.t, G, (int)grid};
+                    fwrite(hdr, sizeof(int), 6, f);
+                    fwrite(h.data(), sizeof(unsigned long long), cnt, f);
+                    fclose(f);
+                }
+                cudaFree(tbuf);
             }
         } else if (pp.v2) {
             bb::PassArgsV2 a2{};

@@ -63,6 +63,7 @@ __device__ __forceinline__ void wait_geq(const int *p, int need)
 {
     if (ld_relaxed(p) < need) {
         while (ld_relaxed(p) < need) {
+            __nanosleep(32);
         }
     }
     fence_acq_rel();

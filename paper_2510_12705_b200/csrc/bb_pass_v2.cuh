@@ -101,9 +101,11 @@ __device__ __forceinline__ void house_thread(const C (&x)[MT], int m, C *v, C &t
         nrm = sqrt(ssq);
     } else {
         C amax = 0;
+#pragma unroll
         for (int k = 0; k < MT; ++k)
             if (k < m) amax = fmax(amax, fabs(x[k]));
         C s2 = 0;
+#pragma unroll
         for (int k = 0; k < MT; ++k)
             if (k < m) {
                 C y = x[k] / amax;
@@ -121,6 +123,7 @@ __device__ __forceinline__ void house_thread(const C (&x)[MT], int m, C *v, C &t
         for (int k = 1; k < MT; ++k)
             if (FULL || k < m) v[k] = x[k] * rcp;
     } else {
+#pragma unroll
         for (int k = 1; k < MT; ++k)
             if (k < m) v[k] = x[k] / den;
     }
