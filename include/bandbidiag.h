@@ -128,8 +128,11 @@ typedef struct {
     double alg_flops;        /* per matrix: sum 4m(hi-q) + 4m(ce-p) + 6m                 */
     int32_t tw;              /* resolved tilewidth                                       */
     int32_t threads_per_block;
-    int64_t ldw;             /* leading dimension of the working band (elements)         */
+    int64_t ldw;             /* leading dimension of the working band (elements),        */
+                             /* >= b_eff + 2 tw + 1, padded so (ldw - 1) * elem is a     */
+                             /* multiple of 16 bytes (TMA diagonal view)                  */
     int64_t ku;              /* storage row of the diagonal in the working band          */
+    int64_t mat_stride;      /* elements between consecutive matrices' working bands    */
     size_t workspace_bytes;  /* bytes bb_workspace_size() would return                   */
 } bb_plan_stats;
 
@@ -148,9 +151,10 @@ bb_status bb_band_to_bidiag_batched(int64_t n, int64_t b, bb_dtype dtype, int64_
  * Workspace layout (documented so tests can inspect the reduced band): it
  * begins with the working band, batch x n columns of ldw elements of the
  * input dtype; matrix k's A(i, j) lives at element
- *     k*n*ldw + (ku + i - j) + j*ldw,   -tw <= j - i <= b_eff + tw
+ *     k*mat_stride + (ku + i - j) + j*ldw,   -tw <= j - i <= b_eff + tw
  * (LAPACK general-band storage with KL = tw, KU = b_eff + tw: the band plus
- * twice the tilewidth of bulge headroom).  ldw and ku come from bb_plan(). */
+ * twice the tilewidth of bulge headroom).  ldw, ku and mat_stride come
+ * from bb_plan(). */
 bb_status bb_band_to_bidiag_ex(int64_t n, int64_t b, bb_dtype dtype, const void *band, int64_t ldband,
                                void *d_out, void *e_out, const bb_config *cfg, void *workspace,
                                size_t workspace_bytes, void *stream);

@@ -43,7 +43,7 @@ class bb_plan_stats(ctypes.Structure):
                 ("critical_cycles", ctypes.c_int64), ("alg_elements", ctypes.c_double),
                 ("alg_bytes", ctypes.c_double), ("alg_flops", ctypes.c_double),
                 ("tw", ctypes.c_int32), ("threads_per_block", ctypes.c_int32),
-                ("ldw", ctypes.c_int64), ("ku", ctypes.c_int64),
+                ("ldw", ctypes.c_int64), ("ku", ctypes.c_int64), ("mat_stride", ctypes.c_int64),
                 ("workspace_bytes", ctypes.c_size_t)]
 
 

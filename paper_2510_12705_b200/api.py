@@ -91,8 +91,9 @@ class Workspace:
     def band_view(self) -> torch.Tensor:
         """Working band after a call: shape (batch, n, ldw), [k, j, ku + i - j] = A_k(i, j)."""
         es = torch.empty(0, dtype=self.dtype).element_size()
-        cnt = self.batch * self.n * self.stats["ldw"]
-        return self.buf[: cnt * es].view(self.dtype).view(self.batch, self.n, self.stats["ldw"])
+        ms, n, ldw = self.stats["mat_stride"], self.n, self.stats["ldw"]
+        flat = self.buf[: self.batch * ms * es].view(self.dtype).view(self.batch, ms)
+        return flat[:, : n * ldw].reshape(self.batch, n, ldw)
 
 
 def band_to_bidiag(band: torch.Tensor, b: int, tw: int | None = None, cfg: Config | None = None,

@@ -8,6 +8,8 @@
 #include "bb_kernels.cuh"
 #include "bb_pass_v2.cuh"
 #include "bb_pass_v3.cuh"
+
+#include <cudaTypedefs.h>
 #include "bandbidiag.h"
 
 #include <algorithm>
@@ -48,14 +50,15 @@ struct PassPlan {
     int mt = 0, ntc = 0, a0 = 0, b0 = 0, LW2 = 0;
     size_t smem2 = 0;
     // multi-sweep kernel (bb_pass_v3.cuh)
-    int g3 = 0, ntg = 0, LDT3 = 0, LDW3 = 0, NS3 = 0;
+    int g3 = 0, ntg = 0, LDT3 = 0, LDW3 = 0, NS3 = 0, nWe3 = 0, WeOff3 = 0, WreOff3 = 0, slot3 = 0;
+    bool tma3 = false;
     size_t smem3 = 0;
 };
 
 struct Plan {
     int64_t n = 0, b_eff = 0, batch = 0;
     int tw = 0;
-    int64_t ldw = 0, ku = 0;
+    int64_t ldw = 0, ku = 0, mat_stride = 0;
     bb_config cfg{};
     std::vector<PassPlan> passes;
     size_t band_bytes = 0, flag_bytes = 0, counter_bytes = 0, total = 0;
@@ -96,6 +99,12 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
     P.tw = tw;
     P.ku = P.b_eff + tw;
     P.ldw = P.b_eff + 2 * tw + 1; // band + twice the tilewidth (reading Q11)
+    {
+        // TMA diagonal view: (ldw - 1) * elem must be a multiple of 16 bytes
+        const int64_t q = 16 / (int64_t)elem_size(dtype);
+        while ((P.ldw - 1) % q) ++P.ldw;
+        P.mat_stride = (n * P.ldw + q - 1) / q * q;
+    }
     P.passes.clear();
     if (n > 2 && P.b_eff > 1) {
         int64_t c = P.b_eff;
@@ -137,14 +146,32 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
                 int G = pp.ntg <= 160 ? 3 : (pp.ntg <= 320 ? 2 : 0);
                 if (const char *e = getenv("BB_V3_G")) G = std::min(G, atoi(e));
                 if (!pp.v2) G = 0;
+                const bool tma = dtype != BB_F16; // slots hold the compute type; TMA copies raw S
+                const int q = tma ? (int)(16 / cs) : 1;
+                auto pitch = [&](int x) {
+                    // bulk copies: multiple of 16 bytes with room for one 16-byte
+                    // misalignment shift; 2 mod 4 elements for fp64 (2-way banks).
+                    // generic fill: odd (conflict-free thread-per-column access)
+                    if (!tma) return round_odd(x);
+                    int v = (x + q + q - 1) / q * q;
+                    if (cs == 8 && (v % 4) == 0) v += 2;
+                    return v;
+                };
+                auto al = [&](size_t elems) { return (elems * cs + 127) / 128 * 128 / cs; };
                 for (; G > 0; --G) {
                     if (c - t < std::max(4, G + 2)) continue;
                     const int WT = (int)t + G;
-                    pp.LDT3 = round_odd((int)c + G);
-                    pp.LDW3 = round_odd(WT);
-                    pp.NS3 = G + 2;
-                    size_t slot = (size_t)pp.LDT3 * WT + (size_t)pp.LDW3 * c;
-                    pp.smem3 = cs * (slot * pp.NS3 + (size_t)G * (2 * pp.mt + 4)) + 16;
+                    pp.LDT3 = pitch((int)c + G);
+                    pp.LDW3 = pitch(WT);
+                    pp.nWe3 = (int)c - 1 - WT;
+                    pp.WeOff3 = (int)al((size_t)pp.LDT3 * WT);
+                    pp.WreOff3 = (int)al((size_t)pp.WeOff3 + (size_t)pp.LDW3 * pp.nWe3);
+                    pp.slot3 = (int)al((size_t)pp.WreOff3 + (size_t)pp.LDW3 * (WT + 1));
+                    pp.tma3 = tma;
+                    for (pp.NS3 = G + 2; pp.NS3 >= G + 1; --pp.NS3) {
+                        pp.smem3 = cs * ((size_t)pp.slot3 * pp.NS3 + (size_t)G * (2 * pp.mt + 4)) + 128;
+                        if (pp.smem3 <= (size_t)kSmemOptinFallback) break;
+                    }
                     if (pp.smem3 <= (size_t)kSmemOptinFallback) break;
                 }
                 pp.g3 = G;
@@ -156,11 +183,27 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
     if (cfg.timing_events && cfg.num_timing_events < (int)P.passes.size() + 3) return BB_ERR_INVALID_VALUE;
     P.cfg = cfg;
     size_t es = elem_size(dtype);
-    P.band_bytes = align_up((size_t)batch * (size_t)n * (size_t)P.ldw * es);
+    P.band_bytes = align_up((size_t)batch * (size_t)P.mat_stride * es);
     P.flag_bytes = align_up((size_t)P.passes.size() * (size_t)batch * (size_t)n * sizeof(int));
     P.counter_bytes = align_up(std::max<size_t>(1, P.passes.size()) * sizeof(int));
     P.total = P.band_bytes + P.flag_bytes + P.counter_bytes;
     return BB_SUCCESS;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder()
+{
+    static std::once_flag once;
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        else
+            cudaGetLastError();
+    });
+    return fn;
 }
 
 struct DeviceInfo {
@@ -204,7 +247,7 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
     S *W = reinterpret_cast<S *>(base);
     int *flags = reinterpret_cast<int *>(base + P.band_bytes);
     int *counters = reinterpret_cast<int *>(base + P.band_bytes + P.flag_bytes);
-    const int64_t mat_stride = P.n * P.ldw;
+    const int64_t mat_stride = P.mat_stride;
     const int n = (int)P.n;
     const int batch = (int)P.batch;
 
@@ -274,13 +317,22 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
             a3.LDT = pp.LDT3;
             a3.LDW = pp.LDW3;
             a3.NS = pp.NS3;
+            a3.nWe = pp.nWe3;
+            a3.WeOff = pp.WeOff3;
+            a3.WreOff = pp.WreOff3;
+            a3.slot_elems = pp.slot3;
             if (const char *e = getenv("BB_V3_DBG")) a3.dbg = atoi(e);
+            // 1-D bulk copies (TMA engine) for the slot fill are opt-in: measured
+            // ~60 cycles per small copy on B200 (tools/ubench/ubench7.cu), slower
+            // than the unrolled coalesced loads for ~130 column segments
+            a3.use_tma = (pp.tma3 && getenv("BB_BULK_FILL")) ? 1 : 0;
             const int nt = G * pp.ntg + 32;
             void (*kern)(bb::PassArgsV3) = nullptr;
 #define BB_PICK3(GG, NTM)                                                                                          \
     kern = pp.mt == 9 ? bb::pass_v3_kernel<S, 9, GG, NTM>                                                         \
                       : (pp.mt == 17 ? bb::pass_v3_kernel<S, 17, GG, NTM> : bb::pass_v3_kernel<S, 33, GG, NTM>)
             if (G == 3) { BB_PICK3(3, 512); }
+            else if (G == 2 && nt <= 352) { BB_PICK3(2, 352); }
             else if (G == 2) { BB_PICK3(2, 672); }
             else { BB_PICK3(1, 352); }
 #undef BB_PICK3
@@ -418,6 +470,14 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
                     fclose(f);
                 }
                 cudaFree(tbuf);
+            }
+        }
+        if (getenv("BB_DEBUG_SYNC")) { // debug: surface asynchronous kernel errors per pass
+            cudaError_t e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) {
+                fprintf(stderr, "bandbidiag: pass %d (c=%d t=%d g3=%d v2=%d) failed: %s\n", (int)pi, pp.c, pp.t,
+                        pp.g3, (int)pp.v2, cudaGetErrorString(e));
+                return BB_ERR_CUDA;
             }
         }
         if (cudaGetLastError() != cudaSuccess) return BB_ERR_CUDA;
@@ -597,6 +657,7 @@ bb_status bb_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const bb_
     out->tw = P.tw;
     out->ldw = P.ldw;
     out->ku = P.ku;
+    out->mat_stride = P.mat_stride;
     out->workspace_bytes = P.total;
     out->threads_per_block = P.passes.empty() ? 0 : P.passes[0].threads;
     double elems = 0, flops = 0;

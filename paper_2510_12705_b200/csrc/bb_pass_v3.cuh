@@ -38,6 +38,8 @@
 
 #include "bb_pass_v2.cuh"
 
+#include <cuda.h> // CUtensorMap
+
 namespace bb {
 
 struct PassArgsV3 {
@@ -54,6 +56,10 @@ struct PassArgsV3 {
     int LDT, LDW;      // slot leading dimensions (odd)
     int NS;            // slots in the ring
     int dbg;           // debug bits (bit 0: generic warp reflector)
+    int nWe;           // early W columns (c - 1 - WT); the last WT + 1 are the right end
+    int WeOff, WreOff; // element offsets of the W parts inside a slot (128-byte aligned)
+    int slot_elems;    // elements per slot (128-byte multiple)
+    int use_tma;       // fill slots with TMA (S == C only)
     unsigned long long *trace;
     int trace_sweeps, trace_steps;
 };
@@ -142,13 +148,78 @@ __device__ __forceinline__ void house_warp_fast(const C *x, int stride, int m, C
 }
 
 template <class C> struct Slot {
-    C *T;  // [LDT * WT]
-    C *W;  // [LDW * c]
+    C *T;   // [LDT * WT]       rows trow0.. of columns p0 .. p0+WT-1
+    C *We;  // [LDW * nWe]      rows p0.. of columns p0+WT .. p0+c-2
+    C *Wre; // [LDW * (WT+1)]   rows p0.. of columns p0+c-1 .. p0+c+WT-1 (right end)
 };
+
+// ---- TMA / mbarrier helpers ------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
+{
+    asm volatile("{\n\t.reg .pred P1;\n"
+                 "WAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+                 "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+                 "r"(parity)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *tm, int x, int y, int z, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+                 "[%5];" ::"r"(smem_u32(dst)),
+                 "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
+__device__ __forceinline__ void mbar_add_tx(uint64_t *bar, unsigned bytes)
+{
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), 16-byte aligned, size multiple of 16
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// Fill `ncol` column segments into shared memory with 1-D bulk copies issued
+// by one warp.  Column k starts (in elements) at g0 + k*gstride in global
+// memory; every start has the same alignment, so each copy starts delta =
+// misalignment elements early and the shared column k begins at
+// s0 + k*spitch (16-byte aligned); the caller addresses it from s0 + delta.
+template <class C>
+__device__ __forceinline__ void bulk_fill_cols(C *s0, int spitch, const C *g0, int64_t gstride, int rows, int ncol,
+                                               int delta, uint64_t *bar, int lane)
+{
+    const int q = 16 / (int)sizeof(C);
+    const unsigned bytes = (unsigned)(((rows + delta + q - 1) / q) * q * sizeof(C));
+    unsigned mine = 0;
+    for (int k = lane; k < ncol; k += 32) mine += bytes;
+    if (mine) mbar_add_tx(bar, mine);
+    __syncwarp();
+    for (int k = lane; k < ncol; k += 32) bulk_g2s(s0 + (size_t)k * spitch, g0 + k * gstride - delta, bytes, bar);
+}
 
 // Geometry of one step (r0+g, j) (q0 of slot j == p0 of slot j-1).
 struct StepGeo {
     int p0, q0, trow0, p, q, hi, ce, m, off, rowsT, ncols;
+    int dT, dW; // bulk-copy misalignment (elements) of the slot's T / W column starts
 };
 
 __device__ __forceinline__ StepGeo step_geo(int n, int c, int t, int G, int r0, int g, int j)
@@ -169,23 +240,26 @@ __device__ __forceinline__ StepGeo step_geo(int n, int c, int t, int G, int r0, 
 }
 
 // shared-memory address of cell (i, jc) of a step in slot j (prev = slot j-1)
+// (the top rows of columns p0..p0+WT-1 live in slot(j-1)'s right-end part)
 template <class C>
 __device__ __forceinline__ C *cell(const StepGeo &s, const Slot<C> &cur, const Slot<C> &prev, int i, int jc, int WT,
-                                   int LDT, int LDW, bool has_prev)
+                                   int LDT, int LDW, bool has_prev, int nWe)
 {
     if (jc < s.p0 + WT) {
-        if (has_prev && i < s.trow0) return prev.W + (i - s.q0) + (jc - s.q0 - WT) * LDW;
+        if (has_prev && i < s.trow0) return prev.Wre + (i - s.q0) + (jc - s.q0 - WT - nWe) * LDW;
         return cur.T + (i - s.trow0) + (jc - s.p0) * LDT;
     }
-    return cur.W + (i - s.p0) + (jc - s.p0 - WT) * LDW;
+    const int k = jc - s.p0 - WT;
+    return (k < nWe ? cur.We + k * LDW : cur.Wre + (k - nWe) * LDW) + (i - s.p0);
 }
 
-template <class S, int MT, bool FULL>
+template <class S, int MT>
 __device__ __forceinline__ void step_v3(const PassArgsV3 &a, S *Wg, int mat, int r0, int g, int G, int j, int Jp,
                                         const int *gprev, int *prog_s, const Slot<typename ComputeOf<S>::type> &cur,
                                         const Slot<typename ComputeOf<S>::type> &prv,
                                         typename ComputeOf<S>::type *v1, typename ComputeOf<S>::type *v2,
-                                        typename ComputeOf<S>::type *scal, int tid, int ntg, int bar, bool wt)
+                                        typename ComputeOf<S>::type *scal, int tid, int ntg, int bar, bool wt_in,
+                                        uint64_t *fbar, unsigned &fphase)
 {
     using C = typename ComputeOf<S>::type;
     const int n = a.n, c = a.c, t = a.t, ku = a.ku;
@@ -193,10 +267,23 @@ __device__ __forceinline__ void step_v3(const PassArgsV3 &a, S *Wg, int mat, int
     const int64_t ldw = a.ldw;
     const int lane = tid & 31, wwarp = tid >> 5;
     const int r = r0 + g;
-    const StepGeo s = step_geo(n, c, t, G, r0, g, j);
-    const int m = FULL ? MT : s.m;
+    StepGeo s = step_geo(n, c, t, G, r0, g, j);
+    {
+        // global column starts: W + ku + row0 + jc*(ldw-1) + mat*mat_stride, with
+        // (ldw-1) and mat_stride multiples of 16 bytes -> same misalignment per slot
+        const int q = 16 / (int)sizeof(C);
+        s.dT = a.use_tma ? (ku + s.trow0) % q : 0;
+        s.dW = a.use_tma ? (ku + s.p0) % q : 0;
+    }
+    // logical slot views (column starts shifted by the bulk-copy misalignment)
+    const int dWp = (a.use_tma && j > 0) ? (ku + s.q0) % (16 / (int)sizeof(C)) : 0; // slot j-1's W shift
+    const Slot<C> cu = {cur.T + s.dT, cur.We + s.dW, cur.Wre + s.dW};
+    const Slot<C> pv = {prv.T, prv.We, prv.Wre + dWp};
+    const int m = s.m;
+    const bool FULL = (m == MT); // full-length reflector: unrolled register loops
     const bool has_prev = j > 0;
     auto gaddr = [&](int i, int jc) -> S * { return Wg + (ku + i - jc) + (int64_t)jc * ldw; };
+    const bool wt = (a.dbg & 2) ? false : wt_in; // debug bit 2: partial write-through only (timing)
 
     // ------------------------------------------------ A wait (+ slot reuse for WG 0)
     if (tid == 0) {
@@ -222,6 +309,26 @@ __device__ __forceinline__ void step_v3(const PassArgsV3 &a, S *Wg, int mat, int
     // Element e -> (column k, row ii) is stepped incrementally (no division per
     // element); every column segment is contiguous in the band, so each warp
     // instruction covers whole segments.
+    if (sizeof(S) == sizeof(C) && a.use_tma) {
+    if (g == 0) {
+        // bulk copies (TMA engine, no registers, one round trip): T part columns
+        // p0 .. p0+WT-1 (rows trow0 ..) and the early W columns (rows p0 ..)
+        if (wwarp == 0) {
+            if (lane == 0) fence_proxy_async(); // generic-proxy accesses before the async copies
+            __syncwarp();
+            const int q = 16 / (int)sizeof(C);
+            const int ncT = min(WT, n - s.p0), ncW = max(0, min(a.nWe, n - s.p0 - WT));
+            bulk_fill_cols<C>(cur.T, LDT, reinterpret_cast<const C *>(gaddr(s.trow0, s.p0)), ldw - 1,
+                              LDT - q, ncT, s.dT, fbar, lane);
+            bulk_fill_cols<C>(cur.We, LDW, reinterpret_cast<const C *>(gaddr(s.p0, s.p0 + WT)), ldw - 1, WT,
+                              ncW, s.dW, fbar, lane);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(fbar);
+        }
+        mbar_wait(fbar, fphase & 1);
+        ++fphase;
+    }
+    } else {
     if (g == 0) {
         const int late0 = (a.b0 > a.a0) ? s.p0 + c - 1 : s.p0 + c + WT;
         const int nWc = max(0, min(late0, s.p0 + c + WT) - (s.p0 + WT));
@@ -231,7 +338,7 @@ __device__ __forceinline__ void step_v3(const PassArgsV3 &a, S *Wg, int mat, int
             const int ncol = part == 0 ? WT : nWc;
             const int i0 = part == 0 ? s.trow0 : s.p0;
             const int j0 = part == 0 ? s.p0 : s.p0 + WT;
-            C *dst0 = part == 0 ? cur.T : cur.W;
+            C *dst0 = part == 0 ? cur.T : cur.We;
             const int ld = part == 0 ? LDT : LDW;
             const int tot = rows * ncol;
             int e = tid, k = e / rows, ii = e - k * rows;
@@ -259,11 +366,12 @@ __device__ __forceinline__ void step_v3(const PassArgsV3 &a, S *Wg, int mat, int
         }
         nbar_sync(bar, ntg);
     }
+    }
     if (tid == 0) TRACE3(2);
 
     // ------------------------------------------------ row reflector (warp 0) from A[q, p..hi]
     // row q lies in slot(j-1).W (j > 0) or slot(0).T
-    C *x0 = cell<C>(s, cur, prv, s.q, s.p, WT, LDT, LDW, has_prev);
+    C *x0 = cell<C>(s, cu, pv, s.q, s.p, WT, LDT, LDW, has_prev, a.nWe);
     const int xs = (has_prev && s.q < s.trow0) ? LDW : LDT;
     if (wwarp == 0) {
         C tau, beta;
@@ -284,22 +392,21 @@ __device__ __forceinline__ void step_v3(const PassArgsV3 &a, S *Wg, int mat, int
     const C tau1 = scal[0];
     for (int ii = 1 + tid; ii < s.rowsT; ii += ntg) {
         const int i = s.q + ii;
-        C *rb = cell<C>(s, cur, prv, i, s.p, WT, LDT, LDW, has_prev);
+        C *rb = cell<C>(s, cu, pv, i, s.p, WT, LDT, LDW, has_prev, a.nWe);
         const int rs = (has_prev && i < s.trow0) ? LDW : LDT;
         S *gb = gaddr(i, s.p);
         const int64_t gs = ldw - 1;
         if (tau1 != C(0)) {
             if (FULL) {
-                C x[MT];
-#pragma unroll
-                for (int k = 0; k < MT; ++k) x[k] = rb[k * rs];
+                // dot product, then a second pass that reloads the row: a small
+                // register footprint (no spills with G warp-groups per SM)
                 C s4[4] = {0, 0, 0, 0};
 #pragma unroll
-                for (int k = 0; k < MT; ++k) s4[k & 3] = fma(x[k], v1[k], s4[k & 3]);
+                for (int k = 0; k < MT; ++k) s4[k & 3] = fma(rb[k * rs], v1[k], s4[k & 3]);
                 const C wv = tau1 * ((s4[0] + s4[1]) + (s4[2] + s4[3]));
 #pragma unroll
                 for (int k = 0; k < MT; ++k) {
-                    const C y = fma(-wv, v1[k], x[k]);
+                    const C y = fma(-wv, v1[k], rb[k * rs]);
                     rb[k * rs] = y;
                     if ((wt || k == 0) && ii < s.off) stg(gb + k * gs, y);
                 }
@@ -325,7 +432,7 @@ __device__ __forceinline__ void step_v3(const PassArgsV3 &a, S *Wg, int mat, int
     }
 
     // ------------------------------------------------ column reflector (warp 0) from A[p..hi, p]
-    C *cp = cell<C>(s, cur, prv, s.p, s.p, WT, LDT, LDW, has_prev); // contiguous over rows p..hi
+    C *cp = cell<C>(s, cu, pv, s.p, s.p, WT, LDT, LDW, has_prev, a.nWe); // contiguous over rows p..hi
     if (wwarp == 0) {
         C tau, beta;
         if ((a.dbg & 1) || sizeof(C) == 4) house_warp<C>(cp, 1, m, v2, tau, beta);
@@ -343,6 +450,22 @@ __device__ __forceinline__ void step_v3(const PassArgsV3 &a, S *Wg, int mat, int
         else wait_geq(gprev, need);
     }
     nbar_sync(bar, ntg);
+    if (sizeof(S) == sizeof(C) && a.use_tma) {
+    if (g == 0 && a.b0 > a.a0) {
+        if (wwarp == 0) {
+            if (lane == 0) fence_proxy_async();
+            __syncwarp();
+            const int jlo = s.p0 + c - 1;
+            const int ncR = max(0, min(WT + 1, n - jlo));
+            bulk_fill_cols<C>(cur.Wre, LDW, reinterpret_cast<const C *>(gaddr(s.p0, jlo)), ldw - 1, WT, ncR,
+                              s.dW, fbar, lane);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(fbar);
+        }
+        mbar_wait(fbar, fphase & 1);
+        ++fphase;
+    }
+    } else {
     if (g == 0 && a.b0 > a.a0) {
         const int jlo = s.p0 + c - 1, jhi = min(s.p0 + c + WT - 1, n - 1);
         const int ncl = jhi - jlo + 1;
@@ -350,9 +473,10 @@ __device__ __forceinline__ void step_v3(const PassArgsV3 &a, S *Wg, int mat, int
             const int k = e / WT, ii = e - k * WT;
             const int i = s.p0 + ii, jc = jlo + k;
             const int rho = ku + i - jc;
-            cur.W[ii + (jc - s.p0 - WT) * LDW] = (i < n && rho >= 0 && rho < ldw) ? ldg_cg(gaddr(i, jc)) : C(0);
+            cur.Wre[ii + k * LDW] = (i < n && rho >= 0 && rho < ldw) ? ldg_cg(gaddr(i, jc)) : C(0);
         }
         nbar_sync(bar, ntg);
+    }
     }
     if (tid == 0) TRACE3(4);
 
@@ -360,17 +484,14 @@ __device__ __forceinline__ void step_v3(const PassArgsV3 &a, S *Wg, int mat, int
     const C tau2 = scal[2];
     if (tau2 != C(0)) {
         for (int sl = 1 + tid; sl < s.ncols; sl += ntg) {
-            C *col = cell<C>(s, cur, prv, s.p, s.p + sl, WT, LDT, LDW, has_prev);
+            C *col = cell<C>(s, cu, pv, s.p, s.p + sl, WT, LDT, LDW, has_prev, a.nWe);
             if (FULL) {
-                C x[MT];
-#pragma unroll
-                for (int kk = 0; kk < MT; ++kk) x[kk] = col[kk];
                 C s4[4] = {0, 0, 0, 0};
 #pragma unroll
-                for (int kk = 0; kk < MT; ++kk) s4[kk & 3] = fma(v2[kk], x[kk], s4[kk & 3]);
+                for (int kk = 0; kk < MT; ++kk) s4[kk & 3] = fma(v2[kk], col[kk], s4[kk & 3]);
                 const C wv = tau2 * ((s4[0] + s4[1]) + (s4[2] + s4[3]));
 #pragma unroll
-                for (int kk = 0; kk < MT; ++kk) col[kk] = fma(-wv, v2[kk], x[kk]);
+                for (int kk = 0; kk < MT; ++kk) col[kk] = fma(-wv, v2[kk], col[kk]);
             } else {
                 C sacc = 0;
                 for (int kk = 0; kk < m; ++kk) sacc = fma(v2[kk], col[kk], sacc);
@@ -389,17 +510,17 @@ __device__ __forceinline__ void step_v3(const PassArgsV3 &a, S *Wg, int mat, int
         const int nw = ntg >> 5;
         for (int sl = wwarp; sl < s.ncols; sl += nw) {
             const int jc = s.p + sl;
-            const C *src = cell<C>(s, cur, prv, s.p, jc, WT, LDT, LDW, has_prev);
+            const C *src = cell<C>(s, cu, pv, s.p, jc, WT, LDT, LDW, has_prev, a.nWe);
             S *dstg = gaddr(s.p, jc);
             for (int kk = lane; kk < m; kk += 32) stg(dstg + kk, src[kk]);
         }
     } else {
         if (wwarp == 0) {
-            const C *src = cell<C>(s, cur, prv, s.p, s.p, WT, LDT, LDW, has_prev);
+            const C *src = cell<C>(s, cu, pv, s.p, s.p, WT, LDT, LDW, has_prev, a.nWe);
             for (int kk = lane; kk < m; kk += 32) stg(gaddr(s.p + kk, s.p) , src[kk]);
         }
         for (int sl = 1 + tid; sl < s.ncols; sl += ntg)
-            stg(gaddr(s.p, s.p + sl), *cell<C>(s, cur, prv, s.p, s.p + sl, WT, LDT, LDW, has_prev));
+            stg(gaddr(s.p, s.p + sl), *cell<C>(s, cu, pv, s.p, s.p + sl, WT, LDT, LDW, has_prev, a.nWe));
     }
     nbar_sync(bar, ntg);
     if (tid == 0) {
@@ -410,20 +531,28 @@ __device__ __forceinline__ void step_v3(const PassArgsV3 &a, S *Wg, int mat, int
 
 // G warp-groups of ntg threads + one RELEASE warp; NS slots in shared memory.
 template <class S, int MT, int G, int NTMAX>
-__global__ void __launch_bounds__(NTMAX, 1) pass_v3_kernel(PassArgsV3 a)
+__global__ void __launch_bounds__(NTMAX, 1)
+    pass_v3_kernel(PassArgsV3 a)
 {
     using C = typename ComputeOf<S>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int s_task;
-    __shared__ int prog_s[G + 1];   // [G] = slots written back by the writer warp
+    __shared__ int prog_s[G + 1];
+    __shared__ __align__(8) uint64_t fill_bar;
+    unsigned fphase = 0;
+    if (threadIdx.x == 0) {
+        mbar_init(&fill_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
 
     const int ntg = a.ntg;
     const int tid_all = threadIdx.x;
     const int g = tid_all / ntg;   // WG index; g == G -> release warp
     const int tid = tid_all - g * ntg;
     const int WT = a.t + G;
-    const size_t slot_elems = (size_t)a.LDT * WT + (size_t)a.LDW * a.c;
-    C *base = reinterpret_cast<C *>(smem_raw);
+    const size_t slot_elems = (size_t)a.slot_elems;
+    // TMA destinations must be 128-byte aligned (the host adds 128 bytes of slack)
+    C *base = reinterpret_cast<C *>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
     C *vbase = base + slot_elems * a.NS;           // per-WG v1, v2, scal
     C *v1 = vbase + (size_t)(g < G ? g : 0) * (2 * MT + 4);
     C *v2 = v1 + MT;
@@ -457,17 +586,13 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v3_kernel(PassArgsV3 a)
                     const bool wt = (g == glast) || (j >= Jnext - 1);
                     Slot<C> cur, prv;
                     cur.T = base + slot_elems * (j % a.NS);
-                    cur.W = cur.T + (size_t)a.LDT * WT;
+                    cur.We = cur.T + a.WeOff;
+                    cur.Wre = cur.T + a.WreOff;
                     prv.T = base + slot_elems * ((j + a.NS - 1) % a.NS);
-                    prv.W = prv.T + (size_t)a.LDT * WT;
-                    const int p = r + (c - t) + j * c;
-                    const int hi = min(p + t, n - 1);
-                    if (hi - p + 1 == MT)
-                        step_v3<S, MT, true>(a, Wg, mat, r0, g, G, j, Jp, gprev, prog_s, cur, prv, v1, v2, scal, tid,
-                                             ntg, 1 + g, wt);
-                    else
-                        step_v3<S, MT, false>(a, Wg, mat, r0, g, G, j, Jp, gprev, prog_s, cur, prv, v1, v2, scal, tid,
-                                              ntg, 1 + g, wt);
+                    prv.We = prv.T + a.WeOff;
+                    prv.Wre = prv.T + a.WreOff;
+                    step_v3<S, MT>(a, Wg, mat, r0, g, G, j, Jp, gprev, prog_s, cur, prv, v1, v2, scal, tid, ntg, 1 + g,
+                                   wt, &fill_bar, fphase);
                 }
             }
         } else if ((tid_all & 31) == 0) {
@@ -482,7 +607,7 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v3_kernel(PassArgsV3 a)
                 const int v = ld_volatile_s(prog_s + glast);
                 if (v > published) {
                     (void)ld_acquire_cta_s(prog_s + glast);
-                    fence_acq_rel();
+                    if (!(a.dbg & 4)) fence_acq_rel(); // debug bit 4: no fence (timing experiments only)
                     asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(gprog + rl), "r"(v) : "memory");
                     published = v;
                 } else if (BB_SPIN_NS) {

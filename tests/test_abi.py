@@ -107,7 +107,10 @@ def test_plan_matches_oracle_enumeration(n, b, dt, tw, es):
     assert st["alg_bytes"] == w["bytes"]
     assert st["alg_flops"] == w["flops"]
     beff = min(b, n - 1)
-    assert st["ldw"] == beff + 2 * st["tw"] + 1      # band + 2 tw headroom
+    assert st["ldw"] >= beff + 2 * st["tw"] + 1      # band + 2 tw headroom
+    assert st["ldw"] <= beff + 2 * st["tw"] + 1 + 16 // es
+    assert ((st["ldw"] - 1) * es) % 16 == 0          # TMA diagonal-view stride
+    assert (st["mat_stride"] * es) % 16 == 0 and st["mat_stride"] >= n * st["ldw"]
     assert st["ku"] == beff + st["tw"]
 
 
