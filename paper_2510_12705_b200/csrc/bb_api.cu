@@ -7,7 +7,7 @@
 // compute entry point returns BB_ERR_CUDA.
 #include "bb_kernels.cuh"
 #include "bb_pass_v2.cuh"
-#include "bb_pass_v3.cuh"
+#include "bb_pass_v4.cuh"
 
 #include <cudaTypedefs.h>
 #include "bandbidiag.h"
@@ -49,10 +49,9 @@ struct PassPlan {
     bool v2 = false;
     int mt = 0, ntc = 0, a0 = 0, b0 = 0, LW2 = 0;
     size_t smem2 = 0;
-    // multi-sweep kernel (bb_pass_v3.cuh)
-    int g3 = 0, ntg = 0, LDT3 = 0, LDW3 = 0, NS3 = 0, nWe3 = 0, WeOff3 = 0, WreOff3 = 0, slot3 = 0;
-    bool tma3 = false;
-    size_t smem3 = 0;
+    // multi-sweep kernel (bb_pass_v4.cuh)
+    int g4 = 0, nt4 = 0, LDT4 = 0, LDW4 = 0, NS4 = 0, slot4 = 0, ntmax4 = 0;
+    size_t smem4 = 0;
 };
 
 struct Plan {
@@ -139,42 +138,38 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
             pp.smem2 = cs * (size_t)(2 * pp.mt + 4 + (size_t)pp.LW2 * (c + t + 1)) + 16;
             pp.v2 = pp.mt > 0 && pp.ntc + 64 <= 512 && !(cfg.flags & BB_FLAG_GENERIC_KERNEL) &&
                     pp.smem2 <= (size_t)kSmemOptinFallback;
-            // multi-sweep CTA (bb_pass_v3.cuh): G warp-groups of ntg threads (+ a release
-            // warp), NS = G + 2 window slots; needs target bandwidth >= max(4, G + 2)
-            pp.ntg = (int)((c + t + 31) / 32 * 32);
+            // multi-sweep CTA (bb_pass_v4.cuh): G warp-groups of nt4 threads + producer and
+            // release warps; needs reflector length t + 1 in {16, 17, 32, 33} (compiled), and
+            // c - t >= max(4, 2G) for G > 1 (bb_pass_v4.cuh header)
             {
-                int G = pp.ntg <= 160 ? 3 : (pp.ntg <= 320 ? 2 : 0);
-                if (const char *e = getenv("BB_V3_G")) G = std::min(G, atoi(e));
-                if (!pp.v2) G = 0;
-                const bool tma = dtype != BB_F16; // slots hold the compute type; TMA copies raw S
-                const int q = tma ? (int)(16 / cs) : 1;
-                auto pitch = [&](int x) {
-                    // bulk copies: multiple of 16 bytes with room for one 16-byte
-                    // misalignment shift; 2 mod 4 elements for fp64 (2-way banks).
-                    // generic fill: odd (conflict-free thread-per-column access)
-                    if (!tma) return round_odd(x);
-                    int v = (x + q + q - 1) / q * q;
-                    if (cs == 8 && (v % 4) == 0) v += 2;
-                    return v;
-                };
-                auto al = [&](size_t elems) { return (elems * cs + 127) / 128 * 128 / cs; };
+                const int MT4 = (int)t + 1;
+                const bool mt_ok = MT4 == 16 || MT4 == 17 || MT4 == 32 || MT4 == 33;
+                pp.nt4 = (int)((c + t + 31) / 32 * 32);
+                pp.ntmax4 = (cs == 8 && MT4 > 17) ? 384 : 576;
+                int gmax = bb::V4_GMAX;
+                if (const char *e = getenv("BB_V4_G")) gmax = std::max(0, std::min(gmax, atoi(e)));
+                if (cfg.flags & BB_FLAG_GENERIC_KERNEL) gmax = 0;
+                int G = mt_ok ? gmax : 0;
                 for (; G > 0; --G) {
-                    if (c - t < std::max(4, G + 2)) continue;
-                    const int WT = (int)t + G;
-                    pp.LDT3 = pitch((int)c + G);
-                    pp.LDW3 = pitch(WT);
-                    pp.nWe3 = (int)c - 1 - WT;
-                    pp.WeOff3 = (int)al((size_t)pp.LDT3 * WT);
-                    pp.WreOff3 = (int)al((size_t)pp.WeOff3 + (size_t)pp.LDW3 * pp.nWe3);
-                    pp.slot3 = (int)al((size_t)pp.WreOff3 + (size_t)pp.LDW3 * (WT + 1));
-                    pp.tma3 = tma;
-                    for (pp.NS3 = G + 2; pp.NS3 >= G + 1; --pp.NS3) {
-                        pp.smem3 = cs * ((size_t)pp.slot3 * pp.NS3 + (size_t)G * (2 * pp.mt + 4)) + 128;
-                        if (pp.smem3 <= (size_t)kSmemOptinFallback) break;
+                    if (G > 1 && (c - t < 4 || c - t < 2 * G)) continue;
+                    if (G * pp.nt4 + 32 * (bb::V4_PW + 1) > pp.ntmax4) continue;
+                    // slot = T (c + G rows, row-major) + W (c columns), both with the
+                    // compile-time pitch TP = (MT | 1) + 8 of bb_pass_v4.cuh
+                    const int TP = (MT4 | 1) + 8;
+                    pp.LDT4 = (int)c + G;
+                    pp.LDW4 = TP;
+                    pp.slot4 = (pp.LDT4 + (int)c) * TP;
+                    pp.slot4 += pp.slot4 & 1;
+                    // dynamic budget leaves room for the kernel's static shared memory
+                    // (progress counters + mbarrier rings, ~2.4 KB)
+                    const size_t budget = (size_t)kSmemOptinFallback - 4096;
+                    for (pp.NS4 = G + 2; pp.NS4 >= G + 1; --pp.NS4) {
+                        pp.smem4 = cs * (size_t)pp.slot4 * pp.NS4;
+                        if (pp.smem4 <= budget) break;
                     }
-                    if (pp.smem3 <= (size_t)kSmemOptinFallback) break;
+                    if (pp.smem4 <= budget && pp.NS4 + 4 <= bb::V4_RING) break;
                 }
-                pp.g3 = G;
+                pp.g4 = G;
             }
             P.passes.push_back(pp);
             c -= t;
@@ -266,7 +261,9 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
             (int)P.ldw, (int)P.ku, n, batch);
     }
     mark(1);
-    for (size_t pi = 0; pi < P.passes.size(); ++pi) {
+    size_t npasses = P.passes.size();
+    if (const char *dp = getenv("BB_DEBUG_PASSES")) npasses = std::min(npasses, (size_t)atoi(dp)); // debug only
+    for (size_t pi = 0; pi < npasses; ++pi) {
         const PassPlan &pp = P.passes[pi];
         if ((int)pp.smem > di.smem_optin) return BB_ERR_NOT_SUPPORTED;
         bb::PassArgs a{};
@@ -296,75 +293,68 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
                 dim3 grid((unsigned)std::max(rmax, 1), (unsigned)batch);
                 kern<<<grid, pp.threads, pp.smem, st>>>(a);
             }
-        } else if (pp.g3 > 0) {
-            const int G = pp.g3;
-            bb::PassArgsV3 a3{};
-            a3.W = W;
-            a3.mat_stride = mat_stride;
-            a3.ldw = (int)P.ldw;
-            a3.ku = (int)P.ku;
-            a3.n = n;
-            a3.c = pp.c;
-            a3.t = pp.t;
-            a3.a0 = pp.a0;
-            a3.b0 = pp.b0;
-            a3.batch = batch;
-            a3.nsweeps = pp.nsweeps;
-            a3.ngroups = (pp.nsweeps + G - 1) / G;
-            a3.progress = a.progress;
-            a3.counter = a.counter;
-            a3.ntg = pp.ntg;
-            a3.LDT = pp.LDT3;
-            a3.LDW = pp.LDW3;
-            a3.NS = pp.NS3;
-            a3.nWe = pp.nWe3;
-            a3.WeOff = pp.WeOff3;
-            a3.WreOff = pp.WreOff3;
-            a3.slot_elems = pp.slot3;
-            if (const char *e = getenv("BB_V3_DBG")) a3.dbg = atoi(e);
-            // 1-D bulk copies (TMA engine) for the slot fill are opt-in: measured
-            // ~60 cycles per small copy on B200 (tools/ubench/ubench7.cu), slower
-            // than the unrolled coalesced loads for ~130 column segments
-            a3.use_tma = (pp.tma3 && getenv("BB_BULK_FILL")) ? 1 : 0;
-            const int nt = G * pp.ntg + 32;
-            void (*kern)(bb::PassArgsV3) = nullptr;
-#define BB_PICK3(GG, NTM)                                                                                          \
-    kern = pp.mt == 9 ? bb::pass_v3_kernel<S, 9, GG, NTM>                                                         \
-                      : (pp.mt == 17 ? bb::pass_v3_kernel<S, 17, GG, NTM> : bb::pass_v3_kernel<S, 33, GG, NTM>)
-            if (G == 3) { BB_PICK3(3, 512); }
-            else if (G == 2 && nt <= 352) { BB_PICK3(2, 352); }
-            else if (G == 2) { BB_PICK3(2, 672); }
-            else { BB_PICK3(1, 352); }
-#undef BB_PICK3
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem3) != cudaSuccess)
+        } else if (pp.g4 > 0) {
+            const int G = pp.g4;
+            bb::PassArgsV4 a4{};
+            a4.W = W;
+            a4.mat_stride = mat_stride;
+            a4.ldw = (int)P.ldw;
+            a4.ku = (int)P.ku;
+            a4.n = n;
+            a4.c = pp.c;
+            a4.t = pp.t;
+            a4.a0 = pp.a0;
+            a4.b0 = pp.b0;
+            a4.batch = batch;
+            a4.nsweeps = pp.nsweeps;
+            a4.G = G;
+            a4.ngroups = (pp.nsweeps + G - 1) / G;
+            a4.progress = a.progress;
+            a4.counter = a.counter;
+            a4.NT = pp.nt4;
+            a4.LDT = pp.LDT4;
+            a4.LDW = pp.LDW4;
+            a4.NS = pp.NS4;
+            a4.slot_elems = pp.slot4;
+            const int nt = G * pp.nt4 + 32 * (bb::V4_PW + 1);
+            void (*kern)(bb::PassArgsV4) = nullptr;
+            switch (pp.t + 1) {
+            case 16: kern = bb::pass_v4_kernel<S, 16, 576>; break;
+            case 17: kern = bb::pass_v4_kernel<S, 17, 576>; break;
+            case 32: kern = sizeof(typename bb::ComputeOf<S>::type) == 8 ? bb::pass_v4_kernel<S, 32, 384>
+                                                                         : bb::pass_v4_kernel<S, 32, 576>; break;
+            default: kern = sizeof(typename bb::ComputeOf<S>::type) == 8 ? bb::pass_v4_kernel<S, 33, 384>
+                                                                          : bb::pass_v4_kernel<S, 33, 576>; break;
+            }
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem4) != cudaSuccess)
                 return BB_ERR_CUDA;
             int occ = 0;
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, pp.smem3) != cudaSuccess)
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, pp.smem4) != cudaSuccess)
                 return BB_ERR_CUDA;
+            if (occ < 1) return BB_ERR_NOT_SUPPORTED;
             if (P.cfg.max_blocks_per_sm > 0) occ = std::min(occ, (int)P.cfg.max_blocks_per_sm);
-            occ = std::max(occ, 1);
-            int64_t tasks = (int64_t)a3.ngroups * batch;
+            int64_t tasks = (int64_t)a4.ngroups * batch;
             int64_t grid = std::min<int64_t>(tasks, (int64_t)occ * di.sms);
             const char *tf = getenv("BB_TRACE_FILE");
             const char *tp = getenv("BB_TRACE_PASS");
             unsigned long long *tbuf = nullptr;
             if (tf && (int)pi == (tp ? atoi(tp) : 0)) {
-                a3.trace_sweeps = std::min(pp.nsweeps, 1024);
-                a3.trace_steps = (int)sweep_len_h(n, pp.c, pp.t, 0);
-                size_t tb = (size_t)a3.trace_sweeps * a3.trace_steps * 16 * sizeof(unsigned long long);
+                a4.trace_sweeps = std::min(pp.nsweeps, 1024);
+                a4.trace_steps = (int)sweep_len_h(n, pp.c, pp.t, 0);
+                size_t tb = (size_t)a4.trace_sweeps * a4.trace_steps * 16 * sizeof(unsigned long long);
                 if (cudaMalloc(&tbuf, tb) == cudaSuccess) {
                     cudaMemsetAsync(tbuf, 0, tb, st);
-                    a3.trace = tbuf;
+                    a4.trace = tbuf;
                 }
             }
-            if (grid >= 1) kern<<<(unsigned)grid, nt, pp.smem3, st>>>(a3);
+            if (grid >= 1) kern<<<(unsigned)grid, nt, pp.smem4, st>>>(a4);
             if (tbuf) {
-                size_t cnt = (size_t)a3.trace_sweeps * a3.trace_steps * 16;
+                size_t cnt = (size_t)a4.trace_sweeps * a4.trace_steps * 16;
                 std::vector<unsigned long long> h(cnt);
                 cudaMemcpyAsync(h.data(), tbuf, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
                 cudaStreamSynchronize(st);
                 if (FILE *f = fopen(tf, "wb")) {
-                    int hdr[6] = {a3.trace_sweeps, a3.trace_steps, pp.c, pp.t, G, (int)grid};
+                    int hdr[6] = {a4.trace_sweeps, a4.trace_steps, pp.c, pp.t, G, (int)grid};
                     fwrite(hdr, sizeof(int), 6, f);
                     fwrite(h.data(), sizeof(unsigned long long), cnt, f);
                     fclose(f);
@@ -475,8 +465,8 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
         if (getenv("BB_DEBUG_SYNC")) { // debug: surface asynchronous kernel errors per pass
             cudaError_t e = cudaStreamSynchronize(st);
             if (e != cudaSuccess) {
-                fprintf(stderr, "bandbidiag: pass %d (c=%d t=%d g3=%d v2=%d) failed: %s\n", (int)pi, pp.c, pp.t,
-                        pp.g3, (int)pp.v2, cudaGetErrorString(e));
+                fprintf(stderr, "bandbidiag: pass %d (c=%d t=%d g4=%d v2=%d) failed: %s\n", (int)pi, pp.c, pp.t,
+                        pp.g4, (int)pp.v2, cudaGetErrorString(e));
                 return BB_ERR_CUDA;
             }
         }
