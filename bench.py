@@ -320,7 +320,7 @@ def main():
     key = f"{a.workload}:{a.n}:{a.b}:{a.dtype}:{a.tw}"
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": ncu_traffic(key), "peak_source": peak_src,
-            "kernel": "pass_flags_kernel (one persistent launch per pass)",
+            "kernel": "pass_v4_kernel (multi-sweep persistent launch per pass; v2 register kernel where v4 does not apply)",
             "alg_bytes_per_step_per_rank": st["alg_bytes"] * B,
             "pass_ms_mean": [float(x) for x in np.mean(np.array(pass_ms), axis=0)],
             "pass_share_of_step": pass_total_ms / ms_per_step}

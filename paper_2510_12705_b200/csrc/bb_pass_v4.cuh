@@ -312,6 +312,36 @@ __device__ __forceinline__ bool refl_scalars(C alpha, C ssq1, C &tau, C &rho, C 
     return true;
 }
 
+// Out-of-line slow path of refl_apply (sum of squares outside the safe
+// range): the same reflector from x scaled by an exact power of two 2^-e
+// (e = exponent of max|x_k|), so no intermediate under/overflows.
+template <class C>
+__device__ __noinline__ C refl_apply_scaled(const C *xb, int xs, int m, C *av, bool has_vec)
+{
+    const C alpha = xb[0];
+    C amax = fabs(alpha);
+    for (int k = 1; k < m; ++k) amax = fmax(amax, fabs(xb[k * xs]));
+    const int e = ilogb(amax);
+    C ss = 0;
+    for (int k = 0; k < m; ++k) {
+        const C yk = scalbn(xb[k * xs], -e);
+        ss = fma(yk, yk, ss);
+    }
+    const C ay = scalbn(alpha, -e);
+    const C nrm_y = sqrt(ss);
+    const C beta_y = ay >= C(0) ? -nrm_y : nrm_y;
+    const C tau = C(1) + fabs(ay) / nrm_y;
+    const C rd = C(1) / (ay - beta_y); // |ay - beta_y| >= nrm_y >= 1
+    if (has_vec) {
+        C sd = av[0];
+        for (int k = 1; k < m; ++k) sd = fma(av[k], scalbn(xb[k * xs], -e) * rd, sd);
+        const C w = tau * sd;
+        av[0] -= w;
+        for (int k = 1; k < m; ++k) av[k] = fma(-w, scalbn(xb[k * xs], -e) * rd, av[k]);
+    }
+    return scalbn(beta_y, e);
+}
+
 // Apply the reflector of the source vector x (shared memory, xb[k*xs],
 // length m; FULL: m == MT) to the register vector av: av -= tau (v . av) v,
 // v_0 = 1, v_k = rho x_k (LAPACK dlarfg reflector, readings Q7/Q8).  The dot
@@ -350,36 +380,13 @@ __device__ __forceinline__ C refl_apply(const C *xb, int m, C (&av)[MT], bool ha
         }
         return beta;
     }
-    // scaled slow path
-    C amax = fabs(alpha);
+    // scaled slow path (out of line: keeps the hot code small for the I-cache)
+    C tmp[MT];
 #pragma unroll
-    for (int k = 1; k < MT; ++k)
-        if (k < m) amax = fmax(amax, fabs(xb[k * xs]));
-    const int e = ilogb(amax);
-    C ss = 0;
+    for (int k = 0; k < MT; ++k) tmp[k] = av[k];
+    beta = refl_apply_scaled<C>(xb, xs, m, tmp, has_vec);
 #pragma unroll
-    for (int k = 0; k < MT; ++k)
-        if (k < m) {
-            const C y = scalbn(xb[k * xs], -e);
-            ss = fma(y, y, ss);
-        }
-    const C ay = scalbn(alpha, -e);
-    const C nrm_y = sqrt(ss);
-    const C beta_y = ay >= C(0) ? -nrm_y : nrm_y;
-    beta = scalbn(beta_y, e);
-    tau = C(1) + fabs(ay) / nrm_y;
-    const C rd = C(1) / (ay - beta_y); // |ay - beta_y| >= nrm_y >= 1
-    if (has_vec) {
-        C sd = av[0];
-#pragma unroll
-        for (int k = 1; k < MT; ++k)
-            if (k < m) sd = fma(av[k], scalbn(xb[k * xs], -e) * rd, sd);
-        const C w = tau * sd;
-        av[0] -= w;
-#pragma unroll
-        for (int k = 1; k < MT; ++k)
-            if (k < m) av[k] = fma(-w, scalbn(xb[k * xs], -e) * rd, av[k]);
-    }
+    for (int k = 0; k < MT; ++k) av[k] = tmp[k];
     return beta;
 }
 
@@ -501,12 +508,18 @@ __device__ __forceinline__ void step_v4(const PassArgsV4 &a, S *Wg, int mat, int
     };
 
     // ---------------------------------------------------------------- A wait
-    if (g == 0) {
-        unsigned par;
-        uint64_t *b = ring_slot(y.barF, y.fbase + j, par);
-        mb_wait(b, par);
+    // one warp waits (hardware-suspended try_wait), the others block on the
+    // WG barrier: waiting warps must not steal issue slots from working ones
+    if (warp == 0) {
+        if (g == 0) {
+            unsigned par;
+            uint64_t *b = ring_slot(y.barF, y.fbase + j, par);
+            mb_wait(b, par);
+        } else {
+            wait_prog(y, g - 1, min(2 * j + a.a0, 2 * Jprev));
+        }
     }
-    else wait_prog(y, g - 1, min(2 * j + a.a0, 2 * Jprev));
+    nbar_sync(bar, NT);
     if (tid == 0) TRACE4(r, j, 0);
 
     // ---------------------------------------------------------------- right application
@@ -568,12 +581,16 @@ __device__ __forceinline__ void step_v4(const PassArgsV4 &a, S *Wg, int mat, int
     }
 
     // ---------------------------------------------------------------- B wait
-    if (g == 0) {
-        unsigned par;
-        uint64_t *b = ring_slot(y.barF + V4_RING, y.fbase + j, par);
-        mb_wait(b, par);
+    if (warp == 0) {
+        if (g == 0) {
+            unsigned par;
+            uint64_t *b = ring_slot(y.barF + V4_RING, y.fbase + j, par);
+            mb_wait(b, par);
+        } else {
+            wait_prog(y, g - 1, min(2 * j + a.b0, 2 * Jprev));
+        }
     }
-    else wait_prog(y, g - 1, min(2 * j + a.b0, 2 * Jprev));
+    nbar_sync(bar, NT);
     if (tid == 0) TRACE4(r, j, 3);
 
     // ---------------------------------------------------------------- left application
@@ -620,16 +637,23 @@ __device__ __forceinline__ void step_v4(const PassArgsV4 &a, S *Wg, int mat, int
         // step j+1 its A write-back there (program order) covers them;
         // otherwise every other WG's A(j+1) write-back happened before (chain)
         // and this copy is the last one.  Own y column from registers.
+        // flattened over the WG: every lane busy (one warp per 19-row column
+        // segment was measured 3x slower, tools/ubench/wbfill.cu)
         const int ncol = own_next ? c : WT + c;
-        for (int k = warp; k < ncol; k += nwarps) {
-            const int jc = s.p0 + k;
-            if (jc >= n) break;
-            const int rlo = max(s.p0, jc - c - t), rhi = min(min(s.p0 + WT - 1, jc + t), n - 1);
-            S *gcol = Wg + (ku - jc) + (int64_t)jc * ldw;
-            for (int i = rlo + lane; i <= rhi; i += 32) {
-                C v = k < WT ? curT[(i - s.trow0) * TP + k] : curW[(k - WT) * TP + (i - s.p0)];
+        const int tot = WT * ncol, dk = NT / WT, dii = NT - dk * WT;
+        int k = tid / WT, ii = tid - k * WT;
+        for (int e = tid; e < tot; e += NT) {
+            const int i = s.p0 + ii, jc = s.p0 + k, off = jc - i;
+            if (i < n && jc < n && off >= -t && off <= c + t) {
+                C v = k < WT ? curT[(i - s.trow0) * TP + k] : curW[(k - WT) * TP + ii];
                 if (jc == s.p && i >= s.p && i <= s.hi) v = (i == s.p) ? beta2 : C(0);
-                stg(gcol + i, v);
+                stg(Wg + (ku + i) + (int64_t)jc * (ldw - 1), v);
+            }
+            ii += dii;
+            k += dk;
+            if (ii >= WT) {
+                ii -= WT;
+                ++k;
             }
         }
         nbar_sync(bar, NT);
@@ -638,6 +662,16 @@ __device__ __forceinline__ void step_v4(const PassArgsV4 &a, S *Wg, int mat, int
         post_prog(y, g, 2 * j + 2);
         TRACE4(r, j, 5);
     }
+}
+
+// Clipped steps at the matrix end (m < MT): out of line, so the hot code
+// (one full step) stays small enough for the instruction cache.
+template <class S, int MT>
+__device__ __noinline__ void step_v4_tail(const PassArgsV4 &a, S *Wg, int mat, int r0, int g, int j, int Jprev,
+                                          bool closer, bool own_next, const SyncV4 &y,
+                                          typename ComputeOf<S>::type *slots, int tid, int bar)
+{
+    step_v4<S, MT, false>(a, Wg, mat, r0, g, j, Jprev, closer, own_next, y, slots, tid, bar);
 }
 
 // G compute WGs of NT threads, V4_PW producer warps, one release warp.
@@ -705,14 +739,12 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v4_kernel(PassArgsV4 a)
                     if (min(p + t, n - 1) - p + 1 == MT)
                         step_v4<S, MT, true>(a, Wg, mat, r0, g, j, Jprev, closer, own_next, y, slots, tid, 1 + g);
                     else
-                        step_v4<S, MT, false>(a, Wg, mat, r0, g, j, Jprev, closer, own_next, y, slots, tid, 1 + g);
+                        step_v4_tail<S, MT>(a, Wg, mat, r0, g, j, Jprev, closer, own_next, y, slots, tid, 1 + g);
                 }
             }
         } else if ((int)threadIdx.x < ncomp + npt) {
             // ------------------------------------------------ PRODUCER warps: fill slot j for the group
-            // one warp per column segment (coalesced global reads, async copies)
             const int ptid = threadIdx.x - ncomp;
-            const int pw = ptid >> 5, lane = ptid & 31;
             const int pbar = 1 + V4_GMAX; // named barrier of the producer warps
             const int J0 = sweep_len(n, c, t, r0);
             const int Jp = r0 > 0 ? sweep_len(n, c, t, r0 - 1) : 0;
@@ -722,14 +754,23 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v4_kernel(PassArgsV4 a)
             const int kLate = max(0, c - t - 2 * G);
             const int ku = a.ku;
             const int64_t ldw = a.ldw;
-            auto fill_w = [&](C *curW, int p0, int k0, int k1) {
-                for (int k = k0 + pw; k < k1; k += V4_PW) {
-                    const int jc = p0 + WT + k;
-                    if (jc >= n) break;
-                    const int rlo = max(p0, jc - c - t), rhi = min(min(p0 + WT - 1, jc + t), n - 1);
-                    const S *gcol = Wg + (ku - jc) + (int64_t)jc * ldw;
-                    C *scol = curW + k * TP - p0;
-                    for (int i = rlo + lane; i <= rhi; i += 32) Fill<S, C>::elem(scol + i, gcol + i);
+            // flattened copy of rows [i0, i0+nr) x cols [c0, c0+nc) (band offsets
+            // [-t, c+t], inside the matrix) to dst[ii*drs + k*dcs]: consecutive
+            // threads on consecutive rows (coalesced), every lane busy
+            auto fill_rect = [&](int i0, int nr, int c0, int nc, C *dst, int drs, int dcs) {
+                if (nr <= 0 || nc <= 0) return;
+                const int tot = nr * nc, dk = npt / nr, dii = npt - dk * nr;
+                int k = ptid / nr, ii = ptid - k * nr;
+                for (int e = ptid; e < tot; e += npt) {
+                    const int i = i0 + ii, jc = c0 + k, off = jc - i;
+                    if (i < n && jc < n && off >= -t && off <= c + t)
+                        Fill<S, C>::elem(dst + ii * drs + k * dcs, Wg + (ku + i) + (int64_t)jc * (ldw - 1));
+                    ii += dii;
+                    k += dk;
+                    if (ii >= nr) {
+                        ii -= nr;
+                        ++k;
+                    }
                 }
             };
             for (int j = 0; j < J0; ++j) {
@@ -747,27 +788,21 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v4_kernel(PassArgsV4 a)
                     TRACE4(r0, j, 6);
                 }
                 nbar_sync(pbar, npt);
-                // T part: rows [trow0, p0 + WT) x cols [p0, p0 + WT), row-major in shared memory
-                for (int k = pw; k < WT; k += V4_PW) {
-                    const int jc = s.p0 + k;
-                    if (jc >= n) break;
-                    const int rlo = max(s.trow0, jc - c - t), rhi = min(min(s.p0 + WT - 1, jc + t), n - 1);
-                    const S *gcol = Wg + (ku - jc) + (int64_t)jc * ldw;
-                    C *scol = curT + k - s.trow0 * TP;
-                    for (int i = rlo + lane; i <= rhi; i += 32) Fill<S, C>::elem(scol + i * TP, gcol + i);
-                }
-                fill_w(curW, s.p0, 0, kLate);
+                // T part first (all WG 0's A phase needs): rows [trow0, p0 + WT) x
+                // cols [p0, p0 + WT), row-major in shared memory
+                fill_rect(s.trow0, s.p0 + WT - s.trow0, s.p0, WT, curT, TP, 1);
                 fill_arrive<S, C>(fA); // completes when every producer thread's copies landed
+                if (ptid == 0) TRACE4(r0, j, 7);
+                // early W columns [p0 + WT, p0 + WT + kLate): only needed by B phases
+                fill_rect(s.p0, WT, s.p0 + WT, kLate, curW, 1, TP);
                 if (pprev && a.b0 > a.a0) {
-                    if (ptid == 0) {
-                        TRACE4(r0, j, 7);
-                        wait_geq_v4(pprev, min(2 * j + a.b0, 2 * Jp), 2 * j + 1, prog_s, r0, glast);
-                    }
+                    if (ptid == 0) wait_geq_v4(pprev, min(2 * j + a.b0, 2 * Jp), 2 * j + 1, prog_s, r0, glast);
                     nbar_sync(pbar, npt);
                 }
                 if (ptid == 0) TRACE4(r0, j, 8);
-                fill_w(curW, s.p0, kLate, c);
+                fill_rect(s.p0, WT, s.p0 + WT + kLate, c - kLate, curW + kLate * TP, 1, TP);
                 fill_arrive<S, C>(fB);
+                if (ptid == 0) TRACE4(r0, j, 9);
             }
             if (Fill<S, C>::async) cp_async_wait_all();
         } else if ((threadIdx.x & 31) == 0) {

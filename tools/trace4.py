@@ -38,12 +38,13 @@ def med(x, m):
     return "median %7d  p10 %7d  p90 %7d" % (np.median(x), np.percentile(x, 10), np.percentile(x, 90)) if x.size else "-"
 print("PROD fill_start - prev step_pub(j)      ", med(P[:, :, 6] - prev[:, :, 5], okp))
 print("PROD fillT duration                     ", med(P[:, :, 7] - P[:, :, 6], okp))
+print("PROD late fill (8 -> 9)                 ", med(P[:, :, 9] - P[:, :, 8], okp))
 if prev1 is not None:
     okq = (P[:, :, 8] > 0) & (prev1[:, :, 2] > 0)
     print("PROD late_go - prev A_pub(j+1)          ", med(P[:, :, 8] - prev1[:, :, 2], okq))
-print("PROD late fill duration                 ", med(P[:, :, 9] - P[:, :, 8], okp))
-print("WG0 A_go - fillT done                   ", med(P[:, :, 0] - P[:, :, 7], okp))
-print("WG0 B_go - late done                    ", med(P[:, :, 3] - P[:, :, 9], okp))
+
+print("WG0 A_go - fillT issued                 ", med(P[:, :, 0] - P[:, :, 7], okp))
+print("WG0 B_go - late issued                  ", med(P[:, :, 3] - P[:, :, 9], okp))
 print("WG0 A_go - prev group step_pub(j)       ", med(P[:, :, 0] - prev[:, :, 5], okp))
 for g in range(1, G):
     rr = rows + g
