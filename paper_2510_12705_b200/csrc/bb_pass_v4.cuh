@@ -482,7 +482,7 @@ __device__ __forceinline__ void wait_geq_v4(const int *p, int need, int dbg_tag,
     fence_acq_rel();
 }
 
-template <class S, int MT, bool FULL>
+template <class S, int MT, bool FULL, bool JP>
 __device__ __forceinline__ void step_v4(const PassArgsV4 &a, S *Wg, int mat, int r0, int g, int j, int Jprev,
                                         bool closer, bool own_next, const SyncV4 &y,
                                         typename ComputeOf<S>::type *slots, int tid, int bar)
@@ -500,7 +500,7 @@ __device__ __forceinline__ void step_v4(const PassArgsV4 &a, S *Wg, int mat, int
     C *curT = slots + (size_t)(j % a.NS) * a.slot_elems;
     C *curW = curT + a.LDT * TP;
     C *prvW = slots + (size_t)((j + a.NS - 1) % a.NS) * a.slot_elems + a.LDT * TP;
-    const bool jp = j > 0;
+    const bool jp = JP || j > 0; // JP: the hot instantiation (full step, j > 0)
     // home of cell (i, jc), jc in [p0, p0 + WT): previous slot's W (rows < trow0) or T
     auto tcell = [&](int i, int jc) -> C * {
         if (jp && i < s.trow0) return prvW + (jc - s.q0 - WT) * TP + (i - s.q0);
@@ -542,7 +542,8 @@ __device__ __forceinline__ void step_v4(const PassArgsV4 &a, S *Wg, int mat, int
 #pragma unroll
             for (int k = 0; k < MT; ++k) av[k] = C(0);
         }
-        beta1 = jp ? refl_apply<C, MT, FULL, TP>(xb, m, av, mine) : refl_apply<C, MT, FULL, 1>(xb, m, av, mine);
+        if (JP) beta1 = refl_apply<C, MT, FULL, TP>(xb, m, av, mine);
+        else beta1 = jp ? refl_apply<C, MT, FULL, TP>(xb, m, av, mine) : refl_apply<C, MT, FULL, 1>(xb, m, av, mine);
         if (mine) {
             if (rprev) st_vec<TP, S, C, MT, FULL>(rb, m, av);
             else st_vec<1, S, C, MT, FULL>(rb, m, av);
@@ -664,14 +665,15 @@ __device__ __forceinline__ void step_v4(const PassArgsV4 &a, S *Wg, int mat, int
     }
 }
 
-// Clipped steps at the matrix end (m < MT): out of line, so the hot code
-// (one full step) stays small enough for the instruction cache.
+// Clipped steps at the matrix end (m < MT) and every sweep's first step
+// (j = 0, x in T): out of line, so the hot code (one full step with j > 0)
+// stays small enough for the instruction cache.
 template <class S, int MT>
 __device__ __noinline__ void step_v4_tail(const PassArgsV4 &a, S *Wg, int mat, int r0, int g, int j, int Jprev,
                                           bool closer, bool own_next, const SyncV4 &y,
                                           typename ComputeOf<S>::type *slots, int tid, int bar)
 {
-    step_v4<S, MT, false>(a, Wg, mat, r0, g, j, Jprev, closer, own_next, y, slots, tid, bar);
+    step_v4<S, MT, false, false>(a, Wg, mat, r0, g, j, Jprev, closer, own_next, y, slots, tid, bar);
 }
 
 // G compute WGs of NT threads, V4_PW producer warps, one release warp.
@@ -736,8 +738,8 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v4_kernel(PassArgsV4 a)
                     const bool closer = (g == glast) || (j >= Jnext);
                     const bool own_next = j + 1 < J;
                     const int p = r + (c - t) + j * c;
-                    if (min(p + t, n - 1) - p + 1 == MT)
-                        step_v4<S, MT, true>(a, Wg, mat, r0, g, j, Jprev, closer, own_next, y, slots, tid, 1 + g);
+                    if (j > 0 && min(p + t, n - 1) - p + 1 == MT)
+                        step_v4<S, MT, true, true>(a, Wg, mat, r0, g, j, Jprev, closer, own_next, y, slots, tid, 1 + g);
                     else
                         step_v4_tail<S, MT>(a, Wg, mat, r0, g, j, Jprev, closer, own_next, y, slots, tid, 1 + g);
                 }
