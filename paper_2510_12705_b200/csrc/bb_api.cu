@@ -51,6 +51,7 @@ struct PassPlan {
     size_t smem2 = 0;
     // multi-sweep kernel (bb_pass_v4.cuh)
     int g4 = 0, nt4 = 0, LDT4 = 0, LDW4 = 0, NS4 = 0, slot4 = 0, ntmax4 = 0;
+    int a4 = 0, b4 = 0; // v4 half-step wait offsets (refined for target bandwidth < 4, tools/depcheck.py)
     size_t smem4 = 0;
 };
 
@@ -170,6 +171,13 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
                     if (pp.smem4 <= budget && pp.NS4 + 4 <= bb::V4_RING) break;
                 }
                 pp.g4 = G;
+                // half-step rule of the v4 kernel (every pair of conflicting phases
+                // ordered, tools/depcheck.py): target bandwidth >= 4: A(j) waits for
+                // progress[r-1] >= 2j+2, B(j) for >= 2j+3; 2..3: 2j+2 / 2j+4 (whole
+                // step s = 2 would be 2j+4 / 2j+4); 1: 2j+4 / 2j+5 (s = 3: 2j+6 / 2j+6)
+                pp.a4 = tb >= 2 ? 2 : 4;
+                pp.b4 = tb >= 4 ? 3 : (tb >= 2 ? 4 : 5);
+                if (pp.s > (tb == 1 ? 3 : 2)) pp.a4 = pp.b4 = 2 * pp.s; // user asked for a larger distance
             }
             P.passes.push_back(pp);
             c -= t;
@@ -303,8 +311,8 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
             a4.n = n;
             a4.c = pp.c;
             a4.t = pp.t;
-            a4.a0 = pp.a0;
-            a4.b0 = pp.b0;
+            a4.a0 = pp.a4;
+            a4.b0 = pp.b4;
             a4.batch = batch;
             a4.nsweeps = pp.nsweeps;
             a4.G = G;

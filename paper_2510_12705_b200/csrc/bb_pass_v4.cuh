@@ -751,9 +751,12 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v4_kernel(PassArgsV4 a)
             const int J0 = sweep_len(n, c, t, r0);
             const int Jp = r0 > 0 ? sweep_len(n, c, t, r0 - 1) : 0;
             const int *pprev = r0 > 0 ? gprog + (r0 - 1) : nullptr;
-            // first late W column index (col >= p0 + c - G); 0 when c - t < 2G (G = 1,
-            // whole-step distance: every column after the single wait)
-            const int kLate = max(0, c - t - 2 * G);
+            // first late W column index: the columns the previous group's phase
+            // awaited by B (and not by A) can still modify.  Refined rule (b0 = 3):
+            // its A(j+1), cols >= p0 + c - G; b0 = 4 (target bandwidth 2..3, G = 1):
+            // its step j+1, cols >= p0 + c - 1; b0 = 5 (target bandwidth 1, G = 1):
+            // its A(j+2), cols >= p0 + 2c - 1.  Equal waits: no late part.
+            const int kLate = (a.b0 == a.a0) ? c : (a.b0 == 5 ? 2 * c - 1 - WT : c - t - 2 * G);
             const int ku = a.ku;
             const int64_t ldw = a.ldw;
             // flattened copy of rows [i0, i0+nr) x cols [c0, c0+nc) (band offsets
