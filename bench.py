@@ -33,7 +33,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 ES = {"f16": 2, "f32": 4, "f64": 8}
-DEFAULT_TW = {"f16": 32, "f32": 32, "f64": 16}
+DEFAULT_TW = {"f16": 32, "f32": 32, "f64": 32}
 
 
 def parse():

@@ -100,7 +100,7 @@ typedef enum {
 /* Tuning knobs, the paper's hyperparameter triple.
  * Zero-initialise for defaults. */
 typedef struct {
-    int32_t tw;                /* inner tilewidth TW; 0 = per-dtype default     */
+    int32_t tw;                /* inner tilewidth TW; 0 = default (32, measured) */
     int32_t threads_per_block; /* "Threads per block"; 0 = auto                 */
     int32_t max_blocks_per_sm; /* "Max blocks": resident CTAs per SM; 0 = auto  */
     int32_t dep_distance;      /* s; 0 = auto (2, or 3 when the pass target is 1);      */

@@ -66,8 +66,12 @@ struct Plan {
 
 int default_tw(bb_dtype dt)
 {
-    // optimum = one 128-byte cache line: 32 (FP32), 16 (FP64).
-    return dt == BB_F64 ? 16 : 32;
+    // P:315 found one 128-byte cache line optimal on its GPUs: 32 (FP32), 16
+    // (FP64).  On B200 with the v4 kernel tw = 32 is faster for FP64 too
+    // (n = 32768, b = 128: 2.2 s vs 2.6 s): the number of
+    // passes -- each a chain of ~n sweep hand-offs -- halves.
+    (void)dt;
+    return 32;
 }
 
 int64_t sweep_len_h(int64_t n, int64_t c, int64_t t, int64_t r)

@@ -182,3 +182,33 @@ def test_known_spectrum_accuracy(dtype, bound, kind):
     d, e = gpu_reduce(band, b, tw=4)
     s = bidiag_svals(d.astype(np.float64), e.astype(np.float64))
     assert np.max(np.abs(s - np.sort(sig)[::-1])) / np.max(sig) < bound
+
+
+# ------------------------------------------------ v4 multi-sweep kernel: G warp-groups per CTA
+@pytest.mark.parametrize("dtype,n,b,tw", [("f64", 900, 128, 16), ("f64", 700, 64, 32), ("f32", 1000, 96, 32),
+                                          ("f16", 800, 64, 32), ("f32", 1300, 128, 16)])
+def test_v4_bitwise_identical_across_group_size(dtype, n, b, tw, monkeypatch):
+    # the multi-sweep kernel hands data from sweep to sweep in shared memory
+    # (G > 1) or through the working band (G = 1); the result must not depend
+    # on it, and it must match the oracle
+    ref = None
+    for G in ("1", "2", "3", "8"):
+        monkeypatch.setenv("BB_V4_G", G)
+        band = synth.random_band(n, b, dtype, seed=40)
+        d, e = gpu_reduce(band, b, tw=tw)
+        if ref is None:
+            ref = (d, e)
+            compare(band, b, tw, dtype, d, e, svals=(dtype != "f16"))
+        else:
+            assert np.array_equal(ref[0], d) and np.array_equal(ref[1], e), G
+
+
+def test_v4_vs_register_kernel_same_tolerance(monkeypatch):
+    # v4 (default) and the v2 register kernel (BB_V4_G=0) both match the oracle
+    n, b, tw = 1200, 128, 16
+    band = synth.random_band(n, b, "f64", seed=41)
+    d4, e4 = gpu_reduce(band, b, tw=tw)
+    monkeypatch.setenv("BB_V4_G", "0")
+    d2, e2 = gpu_reduce(band, b, tw=tw)
+    compare(band, b, tw, "f64", d4, e4)
+    compare(band, b, tw, "f64", d2, e2)
