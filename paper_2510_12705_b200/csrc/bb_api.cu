@@ -50,7 +50,7 @@ struct PassPlan {
     int mt = 0, ntc = 0, a0 = 0, b0 = 0, LW2 = 0;
     size_t smem2 = 0;
     // multi-sweep kernel (bb_pass_v4.cuh)
-    int g4 = 0, nt4 = 0, LDT4 = 0, LDW4 = 0, NS4 = 0, slot4 = 0, ntmax4 = 0;
+    int g4 = 0, nt4 = 0, LDT4 = 0, LDW4 = 0, NS4 = 0, slot4 = 0, ntmax4 = 0, tp4 = 0;
     int a4 = 0, b4 = 0; // v4 half-step wait offsets (refined for target bandwidth < 4, tools/depcheck.py)
     size_t smem4 = 0;
 };
@@ -150,17 +150,27 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
                 const int MT4 = (int)t + 1;
                 const bool mt_ok = MT4 == 16 || MT4 == 17 || MT4 == 32 || MT4 == 33;
                 pp.nt4 = (int)((c + t + 31) / 32 * 32);
-                pp.ntmax4 = (cs == 8 && MT4 > 17) ? 384 : 576;
-                int gmax = bb::V4_GMAX;
+                // instantiated thread bounds: 576 (96 registers); fp64 with t >= 31
+                // needs more registers per thread: 384 (168 registers) or 512 (128)
+                // (the 512 variant spills; measured no faster than G = 1, so fp64 t >= 31
+                // stays within 384 threads)
+                const int ntlim = (cs == 8 && MT4 > 17) ? 384 : 576;
+                int gmax = 4; // measured: G <= 4 is as fast as larger G (tools/gsweep.py)
                 if (const char *e = getenv("BB_V4_G")) gmax = std::max(0, std::min(gmax, atoi(e)));
                 if (cfg.flags & BB_FLAG_GENERIC_KERNEL) gmax = 0;
                 int G = mt_ok ? gmax : 0;
                 for (; G > 0; --G) {
                     if (G > 1 && (c - t < 4 || c - t < 2 * G)) continue;
-                    if (G * pp.nt4 + 32 * (bb::V4_PW + 1) > pp.ntmax4) continue;
-                    // slot = T (c + G rows, row-major) + W (c columns), both with the
-                    // compile-time pitch TP = (MT | 1) + 8 of bb_pass_v4.cuh
-                    const int TP = (MT4 | 1) + 8;
+                    const int nthr = G * pp.nt4 + 32 * (bb::V4_PW + 1);
+                    if (nthr > ntlim) continue;
+                    pp.ntmax4 = (cs == 8 && MT4 > 17) ? (nthr <= 384 ? 384 : 512) : 576;
+                    // slot = T (c + G rows, row-major) + W (c columns), both with a
+                    // compile-time odd pitch TP >= t + G (bb_pass_v4.cuh): (MT | 1) + 8, or
+                    // (MT | 1) + 2 for fp64 t >= 31 (smaller slots: G = 2 fits 227 KB)
+                    const bool tight = cs == 8 && MT4 >= 32 && (int)t + G <= (MT4 | 1) + 2;
+                    if (cs == 8 && MT4 >= 32 && !tight) continue;
+                    const int TP = (MT4 | 1) + (tight ? 2 : 8);
+                    pp.tp4 = TP;
                     pp.LDT4 = (int)c + G;
                     pp.LDW4 = TP;
                     pp.slot4 = (pp.LDT4 + (int)c) * TP;
@@ -330,13 +340,18 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
             a4.slot_elems = pp.slot4;
             const int nt = G * pp.nt4 + 32 * (bb::V4_PW + 1);
             void (*kern)(bb::PassArgsV4) = nullptr;
+            constexpr bool F64 = sizeof(typename bb::ComputeOf<S>::type) == 8;
             switch (pp.t + 1) {
-            case 16: kern = bb::pass_v4_kernel<S, 16, 576>; break;
-            case 17: kern = bb::pass_v4_kernel<S, 17, 576>; break;
-            case 32: kern = sizeof(typename bb::ComputeOf<S>::type) == 8 ? bb::pass_v4_kernel<S, 32, 384>
-                                                                         : bb::pass_v4_kernel<S, 32, 576>; break;
-            default: kern = sizeof(typename bb::ComputeOf<S>::type) == 8 ? bb::pass_v4_kernel<S, 33, 384>
-                                                                          : bb::pass_v4_kernel<S, 33, 576>; break;
+            case 16: kern = bb::pass_v4_kernel<S, 16, 576, 25>; break;
+            case 17: kern = bb::pass_v4_kernel<S, 17, 576, 25>; break;
+            case 32:
+                kern = !F64 ? bb::pass_v4_kernel<S, 32, 576, 41>
+                            : (pp.ntmax4 <= 384 ? bb::pass_v4_kernel<S, 32, 384, 35> : bb::pass_v4_kernel<S, 32, 512, 35>);
+                break;
+            default:
+                kern = !F64 ? bb::pass_v4_kernel<S, 33, 576, 41>
+                            : (pp.ntmax4 <= 384 ? bb::pass_v4_kernel<S, 33, 384, 35> : bb::pass_v4_kernel<S, 33, 512, 35>);
+                break;
             }
             if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem4) != cudaSuccess)
                 return BB_ERR_CUDA;

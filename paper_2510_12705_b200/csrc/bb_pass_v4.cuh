@@ -434,8 +434,8 @@ __device__ __forceinline__ void for_rect(int i0, int nr, int c0, int nc, int n, 
 }
 
 // One step (r0 + g, j) of a compute WG.  FULL: m == MT.
-// Shared-memory layout of a slot (compute type C), TP = (MT | 1) + 8 (odd,
-// >= t + G for G <= 8, a compile-time pitch so every hot loop addresses
+// Shared-memory layout of a slot (compute type C), pitch TP (odd, >= t + G;
+// (MT | 1) + 8 by default, (MT | 1) + 2 for fp64 t >= 31, a compile-time pitch so every hot loop addresses
 // shared memory as base + immediate):
 //   T: ROW-major,    row i - trow0 (LDT = c + G rows), element jc - p0 (< WT)
 //   W: COLUMN-major, column jc - p0 - WT (c columns),  element i - p0 (< WT)
@@ -443,6 +443,7 @@ __device__ __forceinline__ void for_rect(int i0, int nr, int c0, int nc, int n, 
 // the previous slot's W; a left-application column is strided by TP in T or
 // contiguous in W.  Odd TP keeps both thread-per-row and thread-per-column
 // accesses bank-conflict free.
+// default pitch (room for G <= 8); the host may pick a tighter odd pitch >= t + G
 template <int MT> struct TPitch {
     static constexpr int value = (MT | 1) + 8;
 };
@@ -482,13 +483,12 @@ __device__ __forceinline__ void wait_geq_v4(const int *p, int need, int dbg_tag,
     fence_acq_rel();
 }
 
-template <class S, int MT, bool FULL, bool JP>
+template <class S, int MT, int TP, bool FULL, bool JP>
 __device__ __forceinline__ void step_v4(const PassArgsV4 &a, S *Wg, int mat, int r0, int g, int j, int Jprev,
                                         bool closer, bool own_next, const SyncV4 &y,
                                         typename ComputeOf<S>::type *slots, int tid, int bar)
 {
     using C = typename ComputeOf<S>::type;
-    constexpr int TP = TPitch<MT>::value;
     const int n = a.n, c = a.c, t = a.t, G = a.G, NT = a.NT;
     const int WT = t + G;
     const int ku = a.ku;
@@ -547,6 +547,14 @@ __device__ __forceinline__ void step_v4(const PassArgsV4 &a, S *Wg, int mat, int
         if (mine) {
             if (rprev) st_vec<TP, S, C, MT, FULL>(rb, m, av);
             else st_vec<1, S, C, MT, FULL>(rb, m, av);
+            if (G == 1) {
+                // one sweep per CTA: the union is this step's window, so write the
+                // row through from registers (coalesced across the WG for each k)
+                S *grow = Wg + (ku + i) + (int64_t)s.p * (ldw - 1);
+#pragma unroll
+                for (int k = 0; k < MT; ++k)
+                    if (FULL || k < m) stg(grow + (int64_t)k * (ldw - 1), av[k]);
+            }
         }
     }
     nbar_sync(bar, NT);
@@ -556,9 +564,13 @@ __device__ __forceinline__ void step_v4(const PassArgsV4 &a, S *Wg, int mat, int
         const int xs = jp ? TP : 1;
         xb[0] = beta1;
         for (int k = 1; k < m; ++k) xb[k * xs] = C(0);
+        if (G == 1) {
+            S *gx = Wg + (ku + s.q) + (int64_t)s.p * (ldw - 1);
+            for (int k = 0; k < m; ++k) stg(gx + (int64_t)k * (ldw - 1), k == 0 ? beta1 : C(0));
+        }
         TRACE4(r, j, 1);
     }
-    if (closer) {
+    if (closer && G > 1) {
         // A write-back of the union's right-application region: rows
         // [q0, p0 + WT) x cols [p0, p0 + WT), band offsets [-t, c + t]; one
         // warp per column (coalesced).  This WG's own x row is taken from
@@ -668,20 +680,20 @@ __device__ __forceinline__ void step_v4(const PassArgsV4 &a, S *Wg, int mat, int
 // Clipped steps at the matrix end (m < MT) and every sweep's first step
 // (j = 0, x in T): out of line, so the hot code (one full step with j > 0)
 // stays small enough for the instruction cache.
-template <class S, int MT>
+template <class S, int MT, int TP>
 __device__ __noinline__ void step_v4_tail(const PassArgsV4 &a, S *Wg, int mat, int r0, int g, int j, int Jprev,
                                           bool closer, bool own_next, const SyncV4 &y,
                                           typename ComputeOf<S>::type *slots, int tid, int bar)
 {
-    step_v4<S, MT, false, false>(a, Wg, mat, r0, g, j, Jprev, closer, own_next, y, slots, tid, bar);
+    step_v4<S, MT, TP, false, false>(a, Wg, mat, r0, g, j, Jprev, closer, own_next, y, slots, tid, bar);
 }
 
 // G compute WGs of NT threads, V4_PW producer warps, one release warp.
-template <class S, int MT, int NTMAX>
+template <class S, int MT, int NTMAX, int TP>
 __global__ void __launch_bounds__(NTMAX, 1) pass_v4_kernel(PassArgsV4 a)
 {
     using C = typename ComputeOf<S>::type;
-    constexpr int TP = TPitch<MT>::value;
+    static_assert(TP % 2 == 1 && TP >= MT, "slot pitch: odd, >= t + G");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C *slots = reinterpret_cast<C *>(smem_raw);
     __shared__ int s_task;
@@ -739,9 +751,9 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v4_kernel(PassArgsV4 a)
                     const bool own_next = j + 1 < J;
                     const int p = r + (c - t) + j * c;
                     if (j > 0 && min(p + t, n - 1) - p + 1 == MT)
-                        step_v4<S, MT, true, true>(a, Wg, mat, r0, g, j, Jprev, closer, own_next, y, slots, tid, 1 + g);
+                        step_v4<S, MT, TP, true, true>(a, Wg, mat, r0, g, j, Jprev, closer, own_next, y, slots, tid, 1 + g);
                     else
-                        step_v4_tail<S, MT>(a, Wg, mat, r0, g, j, Jprev, closer, own_next, y, slots, tid, 1 + g);
+                        step_v4_tail<S, MT, TP>(a, Wg, mat, r0, g, j, Jprev, closer, own_next, y, slots, tid, 1 + g);
                 }
             }
         } else if ((int)threadIdx.x < ncomp + npt) {
