@@ -50,7 +50,7 @@ struct PassPlan {
     int mt = 0, ntc = 0, a0 = 0, b0 = 0, LW2 = 0;
     size_t smem2 = 0;
     // multi-sweep kernel (bb_pass_v4.cuh)
-    int g4 = 0, nt4 = 0, LDT4 = 0, LDW4 = 0, NS4 = 0, slot4 = 0, ntmax4 = 0, tp4 = 0;
+    int g4 = 0, nt4 = 0, LDT4 = 0, LDW4 = 0, NS4 = 0, slot4 = 0, ntmax4 = 0, tp4 = 0, pw4 = 0;
     int a4 = 0, b4 = 0; // v4 half-step wait offsets (refined for target bandwidth < 4, tools/depcheck.py)
     size_t smem4 = 0;
 };
@@ -185,6 +185,14 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
                     if (pp.smem4 <= budget && pp.NS4 + 4 <= bb::V4_RING) break;
                 }
                 pp.g4 = G;
+                // producer warps: 2, or -- when shared memory already limits the SM to
+                // one CTA -- as many as the thread bound leaves, up to 6 (fills are on
+                // the cross-CTA critical path)
+                pp.pw4 = bb::V4_PW;
+                if (G > 0 && pp.smem4 > (size_t)kSmemOptinFallback / 2) {
+                    const int left = pp.ntmax4 - G * pp.nt4 - 32;
+                    pp.pw4 = std::max(bb::V4_PW, std::min(6, left / 32));
+                }
                 // half-step rule of the v4 kernel (every pair of conflicting phases
                 // ordered, tools/depcheck.py): target bandwidth >= 4: A(j) waits for
                 // progress[r-1] >= 2j+2, B(j) for >= 2j+3; 2..3: 2j+2 / 2j+4 (whole
@@ -338,7 +346,8 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
             a4.LDW = pp.LDW4;
             a4.NS = pp.NS4;
             a4.slot_elems = pp.slot4;
-            const int nt = G * pp.nt4 + 32 * (bb::V4_PW + 1);
+            a4.pw = pp.pw4;
+            const int nt = G * pp.nt4 + 32 * (pp.pw4 + 1);
             void (*kern)(bb::PassArgsV4) = nullptr;
             constexpr bool F64 = sizeof(typename bb::ComputeOf<S>::type) == 8;
             switch (pp.t + 1) {

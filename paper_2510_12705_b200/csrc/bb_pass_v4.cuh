@@ -67,7 +67,7 @@ namespace bb {
 #endif
 
 constexpr int V4_GMAX = 8;
-constexpr int V4_PW = 2; // producer warps
+constexpr int V4_PW = 2; // producer warps (minimum; the launch may add more: a.pw)
 
 struct PassArgsV4 {
     void *W;
@@ -83,6 +83,7 @@ struct PassArgsV4 {
     int LDT, LDW;   // slot pitches (odd)
     int NS;         // slots in the ring (>= G + 1)
     int slot_elems; // elements per slot: LDT*WT (T) then LDW*c (W)
+    int pw;         // producer warps (>= V4_PW)
     unsigned long long *trace;
     int trace_sweeps, trace_steps;
 };
@@ -480,7 +481,7 @@ __device__ __forceinline__ void wait_geq_v4(const int *p, int need, int dbg_tag,
             }
         }
     }
-    fence_acq_rel();
+    (void)ld_acquire(p); // acquire (no full fence: the producer has no stores to drain)
 }
 
 template <class S, int MT, int TP, bool FULL, bool JP>
@@ -688,7 +689,7 @@ __device__ __noinline__ void step_v4_tail(const PassArgsV4 &a, S *Wg, int mat, i
     step_v4<S, MT, TP, false, false>(a, Wg, mat, r0, g, j, Jprev, closer, own_next, y, slots, tid, bar);
 }
 
-// G compute WGs of NT threads, V4_PW producer warps, one release warp.
+// G compute WGs of NT threads, a.pw producer warps, one release warp.
 template <class S, int MT, int NTMAX, int TP>
 __global__ void __launch_bounds__(NTMAX, 1) pass_v4_kernel(PassArgsV4 a)
 {
@@ -707,7 +708,7 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v4_kernel(PassArgsV4 a)
     const int n = a.n, c = a.c, t = a.t;
     const int WT = t + G;
     const int ncomp = G * NT;
-    const int npt = 32 * V4_PW;
+    const int npt = 32 * a.pw;
     const int total = a.batch * a.ngroups;
     for (int i = threadIdx.x; i < NBAR; i += blockDim.x)
         mb_init(bars + i, i >= 2 * V4_GMAX * V4_RING ? (unsigned)npt : 1u);
