@@ -347,7 +347,7 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
             a4.NS = pp.NS4;
             a4.slot_elems = pp.slot4;
             a4.pw = pp.pw4;
-            const int nt = G * pp.nt4 + 32 * (pp.pw4 + 1);
+            int nt = G * pp.nt4 + 32 * (pp.pw4 + 1);
             void (*kern)(bb::PassArgsV4) = nullptr;
             constexpr bool F64 = sizeof(typename bb::ComputeOf<S>::type) == 8;
             switch (pp.t + 1) {
@@ -368,6 +368,19 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
             if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, pp.smem4) != cudaSuccess)
                 return BB_ERR_CUDA;
             if (occ < 1) return BB_ERR_NOT_SUPPORTED;
+            if (occ >= 2 && a4.pw > 1) {
+                // several CTAs per SM (small c): resident groups bound the wavefront
+                // (each CTA holds its sweeps for ~n/c steps), so trade a producer warp
+                // for occupancy when that admits more CTAs per SM
+                int occ1 = 0;
+                const int nt1 = nt - 32 * (a4.pw - 1);
+                if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, kern, nt1, pp.smem4) == cudaSuccess &&
+                    occ1 > occ) {
+                    occ = occ1;
+                    a4.pw = 1;
+                    nt = nt1;
+                }
+            }
             if (P.cfg.max_blocks_per_sm > 0) occ = std::min(occ, (int)P.cfg.max_blocks_per_sm);
             int64_t tasks = (int64_t)a4.ngroups * batch;
             int64_t grid = std::min<int64_t>(tasks, (int64_t)occ * di.sms);
