@@ -63,7 +63,7 @@
 namespace bb {
 
 #ifndef BB_V4_WATCHDOG
-#define BB_V4_WATCHDOG 1 // debug: trap (with a message) on a wait longer than seconds
+#define BB_V4_WATCHDOG 0 // debug: print a message when a wait exceeds 2 s (hang diagnosis)
 #endif
 
 constexpr int V4_GMAX = 8;
