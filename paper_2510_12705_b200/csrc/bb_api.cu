@@ -93,6 +93,15 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
         return BB_ERR_INVALID_VALUE;
     if (cfg.num_timing_events < 0) return BB_ERR_INVALID_VALUE;
     if (cfg.schedule == BB_SCHED_AUTO) cfg.schedule = BB_SCHED_FLAGS;
+    if (cfg.tw == 0 && elem_size(dtype) == 8) {
+        // default tilewidth 32, unless a pass window would not fit one SM's shared
+        // memory even for the generic kernel (very wide fp64 bands, b >~ 400):
+        // then the paper's fp64 value 16
+        bb_config c32 = cfg;
+        c32.tw = 32;
+        Plan probe;
+        if (make_plan(n, b, dtype, batch, &c32, probe) == BB_ERR_NOT_SUPPORTED) cfg.tw = 16;
+    }
     P.n = n;
     P.batch = batch;
     P.b_eff = n > 0 ? std::min<int64_t>(b, n - 1) : 0;
