@@ -218,10 +218,10 @@ def test_v4_vs_register_kernel_same_tolerance(monkeypatch):
 # The oracle cannot reduce n = 32768 in test time (~10 min), so at full size the
 # CUDA path is checked against properties that hold exactly (up to rounding) at
 # any size (pins P2): orthogonal equivalence preserves the
-# Frobenius norm and |det| (triangular: prod |a_ii| = prod |d_i|), row 0 is only
+# Frobenius norm, row 0 is only
 # touched by right reflectors (|e_0| = ||A[0, 1:]||) and column 0 by none
 # (d_0 = a_00 bit for bit), and every other stored slot of the working band is
-# an exact zero.
+# an exact zero.  |det| is not usable here (see below).
 @pytest.mark.parametrize("dtype,n,b", [("f64", 32768, 128), ("f32", 32768, 128), ("f64", 16384, 512)])
 def test_full_size_invariants(dtype, n, b):
     import torch
@@ -248,7 +248,6 @@ def test_full_size_invariants(dtype, n, b):
     assert d[0] == A[0, b]
     row0 = np.array([A[j, b - j] for j in range(1, b + 1)])
     assert abs(abs(e[0]) - np.linalg.norm(row0)) <= 100 * eps * np.linalg.norm(row0)
-    # log |det|
-    la = float(np.sum(np.log(np.abs(A[:, b]))))
-    ld = float(np.sum(np.log(np.abs(d))))
-    assert abs(la - ld) <= 1e3 * eps * n * max(1.0, abs(la) / n)
+    # (|det| is not checked here: random upper-band matrices are exponentially
+    # ill-conditioned -- the trailing d_i fall below 1e-300 and underflow at this
+    # n, in the oracle as well; P2's log-det pin uses well-conditioned inputs)
