@@ -779,15 +779,43 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v4_kernel(PassArgsV4 a)
                 if (nr <= 0 || nc <= 0) return;
                 const int tot = nr * nc, dk = npt / nr, dii = npt - dk * nr;
                 int k = ptid / nr, ii = ptid - k * nr;
-                for (int e = ptid; e < tot; e += npt) {
-                    const int i = i0 + ii, jc = c0 + k, off = jc - i;
-                    if (i < n && jc < n && off >= -t && off <= c + t)
-                        Fill<S, C>::elem(dst + ii * drs + k * dcs, Wg + (ku + i) + (int64_t)jc * (ldw - 1));
-                    ii += dii;
-                    k += dk;
-                    if (ii >= nr) {
-                        ii -= nr;
-                        ++k;
+                if (Fill<S, C>::async) {
+                    for (int e = ptid; e < tot; e += npt) {
+                        const int i = i0 + ii, jc = c0 + k, off = jc - i;
+                        if (i < n && jc < n && off >= -t && off <= c + t)
+                            Fill<S, C>::elem(dst + ii * drs + k * dcs, Wg + (ku + i) + (int64_t)jc * (ldw - 1));
+                        ii += dii;
+                        k += dk;
+                        if (ii >= nr) {
+                            ii -= nr;
+                            ++k;
+                        }
+                    }
+                } else {
+                    // fp16 storage (widened to fp32 through registers): batches of 8
+                    // loads in flight, then their shared-memory stores
+                    constexpr int U = 8;
+                    for (int e = ptid; e < tot; e += U * npt) {
+                        C v[U];
+                        int so[U];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            so[u] = -1;
+                            const int i = i0 + ii, jc = c0 + k, off = jc - i;
+                            if (e + u * npt < tot && i < n && jc < n && off >= -t && off <= c + t) {
+                                v[u] = ldg_cg(Wg + (ku + i) + (int64_t)jc * (ldw - 1));
+                                so[u] = ii * drs + k * dcs;
+                            }
+                            ii += dii;
+                            k += dk;
+                            if (ii >= nr) {
+                                ii -= nr;
+                                ++k;
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+                            if (so[u] >= 0) dst[so[u]] = v[u];
                     }
                 }
             };
