@@ -391,6 +391,8 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
                 }
             }
             if (P.cfg.max_blocks_per_sm > 0) occ = std::min(occ, (int)P.cfg.max_blocks_per_sm);
+            else if (pp.c - pp.t == 1 && pp.c >= 32 && batch == 1) occ = 1; // measured: the sweep chain of the
+            // target-bandwidth-1 pass (c >= 32) runs faster with one CTA per SM (tools/maxb_sweep.py)
             int64_t tasks = (int64_t)a4.ngroups * batch;
             int64_t grid = std::min<int64_t>(tasks, (int64_t)occ * di.sms);
             const char *tf = getenv("BB_TRACE_FILE");
