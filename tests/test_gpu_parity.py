@@ -251,3 +251,16 @@ def test_full_size_invariants(dtype, n, b):
     # (|det| is not checked here: random upper-band matrices are exponentially
     # ill-conditioned -- the trailing d_i fall below 1e-300 and underflow at this
     # n, in the oracle as well; P2's log-det pin uses well-conditioned inputs)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_v4_batched_interleaving_bitwise_equals_single(dtype):
+    # the batched launch interleaves the sweep groups of all matrices in the
+    # same persistent kernels; each matrix's arithmetic is unchanged
+    n, b, B = 900, 128, 3
+    bands = synth.random_band_batch(B, n, b, dtype, seed=42)
+    d, e = gpu_reduce(bands, b, batched=True)
+    for k in range(B):
+        ds, es = gpu_reduce(bands[k], b)
+        assert np.array_equal(d[k], ds) and np.array_equal(e[k], es), k
+    compare(bands[1], b, 32, dtype, d[1], e[1], svals=False)
