@@ -12,10 +12,11 @@
 //    one row and one column, so the union lives in ONE shared-memory slot; a
 //    WG -> WG hand-off is a shared-memory progress counter and no data moves.
 //    Only every G-th hand-off crosses CTAs (global progress flags + L2).
-//  * a PRODUCER warp fills slot j from L2 with cp.async as soon as the
-//    previous group allows it (its own global waits), so WG 0 never waits on
-//    a global poll or an L2 round trip on its critical path except when the
-//    previous group is genuinely late;
+//  * PRODUCER warps (2..6, a.pw) fill slot j from L2 with flattened cp.async
+//    copies as soon as the previous group allows it (their own global waits):
+//    the T part first (all WG 0's right application needs, signalled on its
+//    own mbarrier), then the early W columns, then -- after the B wait -- the
+//    late W columns;
 //  * the step (Alg. 2) with a short critical path: every thread of the WG
 //    loads the reflector source vector x (row q) itself and computes the
 //    reflector scalars redundantly (beta, tau, rho = 1/(alpha - beta); no
@@ -25,7 +26,8 @@
 //    so they overlap the norm reduction (same reflector as LAPACK dlarfg,
 //    reading Q7; identity iff x[1:] == 0 exactly, reading Q8).  The left
 //    application is the same with the column y = A[p..hi][p].  Two WG
-//    barriers per step.
+//    barriers per step.  With G = 1 the right-application rows are also
+//    written through to the band from registers.
 //  * write-back by the LAST MODIFIER: the "closer" of step j (the last WG of
 //    the group that has a step j) copies the group's whole step-j union to
 //    the working band: the right-application region after its A half (before
@@ -34,21 +36,22 @@
 //    unchanged; nobody else writes them in between (c - t >= 2G, see below).
 //
 // SLOT j (sweep r0's geometry p0 = r0 + (c - t) + j*c, q0 = (j ? p0 - c : r0),
-// WT = t + G, trow0 = (j ? q0 + WT : r0)) holds, column-major in the compute
-// type C:
-//   T: rows [trow0, trow0 + LDT) x cols [p0, p0 + WT)        (pitch LDT, odd)
-//   W: rows [p0, p0 + WT)        x cols [p0 + WT, p0 + WT + c) (pitch LDW, odd)
+// WT = t + G, trow0 = (j ? q0 + WT : r0)) holds, in the compute type C, with
+// a compile-time odd pitch TP >= WT (see "Shared-memory layout" below):
+//   T: rows [trow0, trow0 + c + G) x cols [p0, p0 + WT), row-major
+//   W: rows [p0, p0 + WT) x cols [p0 + WT, p0 + WT + c), column-major
 // Rows [q0, q0 + WT) of cols [p0, p0 + WT) belong to slot j-1's W (its right
 // end), so every cell has exactly one home.  Only cells with band offset
 // col - row in [-t, c + t] (the fill-in bound, reading Q11) are ever loaded,
 // used or written back.
 //
-// ORDERING.  Inside the CTA: WG g waits for WG g-1 with the refined rule
-// (A(j): progress >= 2j + a0, B(j): >= 2j + b0), on shared-memory counters
-// (CTA-scope release/acquire).  Across CTAs (previous group -> WG 0 through
-// the producer): the T part and the early W columns (col < p0 + c - G) of slot
-// j are loaded after the previous group's last sweep published 2j + a0; the
-// late W columns (touched by the previous group's A(j+1)) after 2j + b0.
+// ORDERING.  Inside the CTA: WG g waits for WG g-1 with the half-step rule
+// (A(j): progress >= 2j + a0, B(j): >= 2j + b0; a0/b0 by target bandwidth,
+// bb_api.cu), on shared-memory counters (CTA-scope release/acquire) with
+// mbarrier-based sleeping waits.  Across CTAs (previous group -> WG 0 through
+// the producer): the T part and the early W columns of slot j are loaded
+// after the previous group's last sweep published 2j + a0; the late W columns
+// (those the phase awaited by B can still modify) after 2j + b0.
 // The RELEASE warp republishes the group's last sweep's counter at gpu scope
 // (fence + store); the final value (sweep finished) is only published once
 // every WG of the group finished, so data written back by earlier WGs at the
