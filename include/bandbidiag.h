@@ -68,7 +68,18 @@
 extern "C" {
 #endif
 
-#define BB_VERSION 100 /* 0.1.0 */
+#define BB_VERSION 200 /* 0.2.0: multi-sweep pass kernel (v4), half-step wavefront rules */
+
+/* Diagnostics read from the environment at call time (never needed for normal
+ * use; results are bitwise independent of BB_V4_G):
+ *   BB_V4_G=g          cap the sweeps per CTA of the multi-sweep kernel (0: use the
+ *                      one-sweep register kernel instead)
+ *   BB_TRACE_FILE=f, BB_TRACE_PASS=p
+ *                      dump per-step device timestamps of pass p (tools/trace4.py);
+ *                      synchronises the stream
+ *   BB_DEBUG_SYNC=1    synchronise after every pass and report the failing pass
+ *   BB_DEBUG_PASSES=k  run only the first k passes (the result is then not bidiagonal)
+ *   BB_DEBUG_MAX_CYCLES=k  (cycle schedule only) run only k cycles of each pass */
 
 typedef enum { BB_F16 = 0, BB_F32 = 1, BB_F64 = 2 } bb_dtype;
 

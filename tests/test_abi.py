@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_version_and_status_strings():
-    assert bb.bb_version() == 100
+    assert bb.bb_version() == 200
     for s in range(6):
         assert N.status_string(s).startswith("BB_")
 
