@@ -107,6 +107,8 @@ typedef enum {
 #define BB_FLAG_GENERIC_KERNEL 0x2u /* force the generic shared-memory step kernel (the   */
                                    /* register kernel serves tw <= 32); results are      */
                                    /* bitwise identical, for testing                     */
+#define BB_FLAG_NO_UNIT_KERNEL 0x4u /* never use the unit kernel (G sweeps advanced one step */
+                                    /* at a time, bb_pass_v5.cuh); testing / comparison    */
 
 /* Tuning knobs, the paper's hyperparameter triple.
  * Zero-initialise for defaults. */

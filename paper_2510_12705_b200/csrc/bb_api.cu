@@ -5,11 +5,8 @@
 // Host logic only; every arithmetic step of the method runs in the kernels of
 // bb_kernels.cuh.  No CPU fallback exists: without a usable CUDA device every
 // compute entry point returns BB_ERR_CUDA.
-#include "bb_kernels.cuh"
-#include "bb_pass_v2.cuh"
-#include "bb_pass_v4.cuh"
-
-#include <cudaTypedefs.h>
+#include "bb_plan.h"
+#include "bb_pass_v4.cuh" // constants of the multi-sweep kernel's plan (no kernel is instantiated here)
 #include "bandbidiag.h"
 
 #include <algorithm>
@@ -19,50 +16,7 @@
 #include <mutex>
 #include <vector>
 
-namespace {
-
-constexpr size_t kAlign = 256;
-constexpr int kSmemOptinFallback = 227 * 1024;
-
-inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
-inline int round_odd(int x) { return (x & 1) ? x : x + 1; }
-
-size_t elem_size(bb_dtype dt)
-{
-    switch (dt) {
-    case BB_F16: return 2;
-    case BB_F32: return 4;
-    case BB_F64: return 8;
-    }
-    return 0;
-}
-size_t compute_size(bb_dtype dt) { return dt == BB_F64 ? 8 : 4; }
-
-struct PassPlan {
-    int c, t, s;
-    int nsweeps;     // non-empty sweeps: r in [0, nsweeps)
-    int cycles;      // max_r (s*r + J_r)
-    int LT, LW;
-    size_t smem;     // dynamic shared memory bytes
-    int threads;
-    // register kernel (bb_pass_v2.cuh)
-    bool v2 = false;
-    int mt = 0, ntc = 0, a0 = 0, b0 = 0, LW2 = 0;
-    size_t smem2 = 0;
-    // multi-sweep kernel (bb_pass_v4.cuh)
-    int g4 = 0, nt4 = 0, LDT4 = 0, LDW4 = 0, NS4 = 0, slot4 = 0, ntmax4 = 0, tp4 = 0, pw4 = 0;
-    int a4 = 0, b4 = 0; // v4 half-step wait offsets (refined for target bandwidth < 4, tools/depcheck.py)
-    size_t smem4 = 0;
-};
-
-struct Plan {
-    int64_t n = 0, b_eff = 0, batch = 0;
-    int tw = 0;
-    int64_t ldw = 0, ku = 0, mat_stride = 0;
-    bb_config cfg{};
-    std::vector<PassPlan> passes;
-    size_t band_bytes = 0, flag_bytes = 0, counter_bytes = 0, total = 0;
-};
+namespace bbhost {
 
 int default_tw(bb_dtype dt)
 {
@@ -74,11 +28,6 @@ int default_tw(bb_dtype dt)
     return 32;
 }
 
-int64_t sweep_len_h(int64_t n, int64_t c, int64_t t, int64_t r)
-{
-    int64_t first = r + c - t;
-    return first > n - 2 ? 0 : (n - 2 - first) / c + 1;
-}
 
 bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const bb_config *cfg_in, Plan &P)
 {
@@ -210,6 +159,56 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
                 pp.b4 = tb >= 4 ? 3 : (tb >= 2 ? 4 : 5);
                 if (pp.s > (tb == 1 ? 3 : 2)) pp.a4 = pp.b4 = 2 * pp.s; // user asked for a larger distance
             }
+            // unit kernel (bb_pass_v5.cuh): reflector length t + 1 in {17, 33}, G a
+            // multiple of 8 with G <= c - t (only exactly commuting reflector pairs are
+            // reordered), one unit window + reflector panels in shared memory
+            {
+                const int MT5 = (int)t + 1;
+                const bool ok5 = (MT5 == 17 || MT5 == 33) && !(cfg.flags & (BB_FLAG_GENERIC_KERNEL | BB_FLAG_NO_UNIT_KERNEL)) &&
+                                 pp.s == (tb == 1 ? 3 : 2);
+                int gcap = 32;
+                if (const char *e = getenv("BB_V5_G")) gcap = std::max(0, std::min(32, atoi(e)));
+                // compiled group sizes 32, 16, 8: the largest with 2G <= c - t (the
+                // cheaper wait rule), else the largest with G <= c - t; halved until
+                // the unit window fits shared memory
+                int G = 0;
+                const int VP = (MT5 + 2) & ~1;
+                if (ok5) {
+                    for (int Gc : {32, 16, 8})
+                        if (Gc <= gcap && 2 * Gc <= c - t) {
+                            G = Gc;
+                            break;
+                        }
+                    if (!G)
+                        for (int Gc : {32, 16, 8})
+                            if (Gc <= gcap && Gc <= c - t) {
+                                G = Gc;
+                                break;
+                            }
+                }
+                for (; G >= 8; G /= 2) {
+                    const int W = (int)t + G;
+                    const int LA = round_odd((int)c + W), LB = round_odd(W);
+                    const size_t sm = compute_size(dtype) * ((size_t)W * LA + (size_t)c * LB + 2 * (size_t)G * VP + 2 * (MT5 + 1)) + 16;
+                    if (sm <= (size_t)kSmemOptinFallback - 1024) {
+                        pp.g5 = G;
+                        pp.LA5 = LA;
+                        pp.LB5 = LB;
+                        pp.smem5 = sm;
+                        break;
+                    }
+                }
+                if (pp.g5 > 0) {
+                    // inter-group rule of the unit kernel: exact hazard search over its
+                    // load / write-back rectangles (tools/v5_rules.py): A half waits for
+                    // progress[k-1] >= 2j + a5, B half for >= 2j + b5
+                    const bool tight = 2 * pp.g5 <= c - t;
+                    pp.a5 = tight ? 2 : 4;
+                    pp.b5 = tight ? 4 : 5;
+                    pp.nt5 = (int)std::min<int64_t>(256, std::max<int64_t>(64, (c + t + 31) / 32 * 32));
+                    pp.ngroups5 = (int)((ns + pp.g5 - 1) / pp.g5);
+                }
+            }
             P.passes.push_back(pp);
             c -= t;
         }
@@ -224,27 +223,6 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
     return BB_SUCCESS;
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder()
-{
-    static std::once_flag once;
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    std::call_once(once, [] {
-        void *p = nullptr;
-        cudaDriverEntryPointQueryResult q{};
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-        else
-            cudaGetLastError();
-    });
-    return fn;
-}
-
-struct DeviceInfo {
-    int sms = 0;
-    int smem_optin = 0;
-    bool ok = false;
-};
 
 bool device_info(DeviceInfo &out)
 {
@@ -269,281 +247,6 @@ bool device_info(DeviceInfo &out)
     }
     out = cache[dev];
     return true;
-}
-
-template <class S>
-bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t stride_band, int64_t b_in,
-                     void *d_out, int64_t stride_d, void *e_out, int64_t stride_e, void *ws, cudaStream_t st)
-{
-    DeviceInfo di;
-    if (!device_info(di)) return BB_ERR_CUDA;
-    unsigned char *base = reinterpret_cast<unsigned char *>(ws);
-    S *W = reinterpret_cast<S *>(base);
-    int *flags = reinterpret_cast<int *>(base + P.band_bytes);
-    int *counters = reinterpret_cast<int *>(base + P.band_bytes + P.flag_bytes);
-    const int64_t mat_stride = P.mat_stride;
-    const int n = (int)P.n;
-    const int batch = (int)P.batch;
-
-    cudaEvent_t *ev = reinterpret_cast<cudaEvent_t *>(P.cfg.timing_events);
-    auto mark = [&](int k) { if (ev) cudaEventRecord(ev[k], st); };
-    if (!P.passes.empty()) {
-        if (cudaMemsetAsync(flags, 0, P.flag_bytes + P.counter_bytes, st) != cudaSuccess) return BB_ERR_CUDA;
-    }
-    mark(0);
-    {
-        int64_t total = (int64_t)batch * mat_stride;
-        int thr = 256;
-        int64_t blocks = std::min<int64_t>((total + thr - 1) / thr, (int64_t)di.sms * 16);
-        bb::pack_kernel<S><<<(unsigned)std::max<int64_t>(blocks, 1), thr, 0, st>>>(
-            reinterpret_cast<const S *>(band), ldband, stride_band, (int)b_in, (int)P.b_eff, W, mat_stride,
-            (int)P.ldw, (int)P.ku, n, batch);
-    }
-    mark(1);
-    size_t npasses = P.passes.size();
-    if (const char *dp = getenv("BB_DEBUG_PASSES")) npasses = std::min(npasses, (size_t)atoi(dp)); // debug only
-    for (size_t pi = 0; pi < npasses; ++pi) {
-        const PassPlan &pp = P.passes[pi];
-        if ((int)pp.smem > di.smem_optin) return BB_ERR_NOT_SUPPORTED;
-        bb::PassArgs a{};
-        a.W = W;
-        a.mat_stride = mat_stride;
-        a.ldw = (int)P.ldw;
-        a.ku = (int)P.ku;
-        a.n = n;
-        a.c = pp.c;
-        a.t = pp.t;
-        a.s = pp.s;
-        a.batch = batch;
-        a.nsweeps = pp.nsweeps;
-        a.progress = flags + (int64_t)pi * batch * n;
-        a.counter = counters + pi;
-        a.LT = pp.LT;
-        a.LW = pp.LW;
-        if (P.cfg.schedule == BB_SCHED_CYCLE) {
-            auto kern = bb::pass_cycle_kernel<S>;
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem) != cudaSuccess)
-                return BB_ERR_CUDA;
-            int maxT = pp.cycles;
-            if (const char *dbg = getenv("BB_DEBUG_MAX_CYCLES")) maxT = std::min(maxT, atoi(dbg)); // debug only
-            for (int T = 0; T < maxT; ++T) {
-                a.cycle_T = T;
-                int rmax = std::min(T / pp.s + 1, pp.nsweeps);
-                dim3 grid((unsigned)std::max(rmax, 1), (unsigned)batch);
-                kern<<<grid, pp.threads, pp.smem, st>>>(a);
-            }
-        } else if (pp.g4 > 0) {
-            const int G = pp.g4;
-            bb::PassArgsV4 a4{};
-            a4.W = W;
-            a4.mat_stride = mat_stride;
-            a4.ldw = (int)P.ldw;
-            a4.ku = (int)P.ku;
-            a4.n = n;
-            a4.c = pp.c;
-            a4.t = pp.t;
-            a4.a0 = pp.a4;
-            a4.b0 = pp.b4;
-            a4.batch = batch;
-            a4.nsweeps = pp.nsweeps;
-            a4.G = G;
-            a4.ngroups = (pp.nsweeps + G - 1) / G;
-            a4.progress = a.progress;
-            a4.counter = a.counter;
-            a4.NT = pp.nt4;
-            a4.LDT = pp.LDT4;
-            a4.LDW = pp.LDW4;
-            a4.NS = pp.NS4;
-            a4.slot_elems = pp.slot4;
-            a4.pw = pp.pw4;
-            int nt = G * pp.nt4 + 32 * (pp.pw4 + 1);
-            void (*kern)(bb::PassArgsV4) = nullptr;
-            constexpr bool F64 = sizeof(typename bb::ComputeOf<S>::type) == 8;
-            switch (pp.t + 1) {
-            case 16: kern = bb::pass_v4_kernel<S, 16, 576, 25>; break;
-            case 17: kern = bb::pass_v4_kernel<S, 17, 576, 25>; break;
-            case 32:
-                kern = !F64 ? bb::pass_v4_kernel<S, 32, 576, 41>
-                            : (pp.ntmax4 <= 384 ? bb::pass_v4_kernel<S, 32, 384, 35> : bb::pass_v4_kernel<S, 32, 512, 35>);
-                break;
-            default:
-                kern = !F64 ? bb::pass_v4_kernel<S, 33, 576, 41>
-                            : (pp.ntmax4 <= 384 ? bb::pass_v4_kernel<S, 33, 384, 35> : bb::pass_v4_kernel<S, 33, 512, 35>);
-                break;
-            }
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem4) != cudaSuccess)
-                return BB_ERR_CUDA;
-            int occ = 0;
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, pp.smem4) != cudaSuccess)
-                return BB_ERR_CUDA;
-            if (occ < 1) return BB_ERR_NOT_SUPPORTED;
-            if (occ >= 2 && a4.pw > 1) {
-                // several CTAs per SM (small c): resident groups bound the wavefront
-                // (each CTA holds its sweeps for ~n/c steps), so trade a producer warp
-                // for occupancy when that admits more CTAs per SM
-                int occ1 = 0;
-                const int nt1 = nt - 32 * (a4.pw - 1);
-                if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, kern, nt1, pp.smem4) == cudaSuccess &&
-                    occ1 > occ) {
-                    occ = occ1;
-                    a4.pw = 1;
-                    nt = nt1;
-                }
-            }
-            if (P.cfg.max_blocks_per_sm > 0) occ = std::min(occ, (int)P.cfg.max_blocks_per_sm);
-            else if (pp.c - pp.t == 1 && pp.c >= 32 && batch == 1) occ = 1; // measured: the sweep chain of the
-            // target-bandwidth-1 pass (c >= 32) runs faster with one CTA per SM (tools/maxb_sweep.py)
-            int64_t tasks = (int64_t)a4.ngroups * batch;
-            int64_t grid = std::min<int64_t>(tasks, (int64_t)occ * di.sms);
-            const char *tf = getenv("BB_TRACE_FILE");
-            const char *tp = getenv("BB_TRACE_PASS");
-            unsigned long long *tbuf = nullptr;
-            if (tf && (int)pi == (tp ? atoi(tp) : 0)) {
-                a4.trace_sweeps = std::min(pp.nsweeps, 1024);
-                a4.trace_steps = (int)sweep_len_h(n, pp.c, pp.t, 0);
-                size_t tb = (size_t)a4.trace_sweeps * a4.trace_steps * 16 * sizeof(unsigned long long);
-                if (cudaMalloc(&tbuf, tb) == cudaSuccess) {
-                    cudaMemsetAsync(tbuf, 0, tb, st);
-                    a4.trace = tbuf;
-                }
-            }
-            if (grid >= 1) kern<<<(unsigned)grid, nt, pp.smem4, st>>>(a4);
-            if (tbuf) {
-                size_t cnt = (size_t)a4.trace_sweeps * a4.trace_steps * 16;
-                std::vector<unsigned long long> h(cnt);
-                cudaMemcpyAsync(h.data(), tbuf, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
-                cudaStreamSynchronize(st);
-                if (FILE *f = fopen(tf, "wb")) {
-                    int hdr[6] = {a4.trace_sweeps, a4.trace_steps, pp.c, pp.t, G, (int)grid};
-                    fwrite(hdr, sizeof(int), 6, f);
-                    fwrite(h.data(), sizeof(unsigned long long), cnt, f);
-                    fclose(f);
-                }
-                cudaFree(tbuf);
-            }
-        } else if (pp.v2) {
-            bb::PassArgsV2 a2{};
-            a2.W = W;
-            a2.mat_stride = mat_stride;
-            a2.ldw = (int)P.ldw;
-            a2.ku = (int)P.ku;
-            a2.n = n;
-            a2.c = pp.c;
-            a2.t = pp.t;
-            a2.a0 = pp.a0;
-            a2.b0 = pp.b0;
-            a2.batch = batch;
-            a2.nsweeps = pp.nsweeps;
-            a2.progress = a.progress;
-            a2.counter = a.counter;
-            a2.ntc = pp.ntc;
-            a2.LW = pp.LW2;
-            void (*kern)(bb::PassArgsV2) = nullptr;
-            const int nt = pp.ntc + 64;
-            if (nt <= 256) {
-                kern = pp.mt == 9 ? bb::pass_v2_kernel<S, 9, 256>
-                                  : (pp.mt == 17 ? bb::pass_v2_kernel<S, 17, 256> : bb::pass_v2_kernel<S, 33, 256>);
-            } else {
-                kern = pp.mt == 9 ? bb::pass_v2_kernel<S, 9, 512>
-                                  : (pp.mt == 17 ? bb::pass_v2_kernel<S, 17, 512> : bb::pass_v2_kernel<S, 33, 512>);
-            }
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem2) != cudaSuccess)
-                return BB_ERR_CUDA;
-            int occ = 0;
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, pp.smem2) != cudaSuccess)
-                return BB_ERR_CUDA;
-            if (P.cfg.max_blocks_per_sm > 0) occ = std::min(occ, (int)P.cfg.max_blocks_per_sm);
-            occ = std::max(occ, 1);
-            int64_t tasks = (int64_t)pp.nsweeps * batch;
-            int64_t grid = std::min<int64_t>(tasks, (int64_t)occ * di.sms);
-            const char *tf = getenv("BB_TRACE_FILE");
-            const char *tp = getenv("BB_TRACE_PASS");
-            unsigned long long *tbuf = nullptr;
-            if (tf && (int)pi == (tp ? atoi(tp) : 0)) {
-                a2.trace_sweeps = std::min(pp.nsweeps, 1024);
-                a2.trace_steps = (int)sweep_len_h(n, pp.c, pp.t, 0);
-                size_t tb = (size_t)a2.trace_sweeps * a2.trace_steps * 16 * sizeof(unsigned long long);
-                if (cudaMalloc(&tbuf, tb) == cudaSuccess) {
-                    cudaMemsetAsync(tbuf, 0, tb, st);
-                    a2.trace = tbuf;
-                }
-            }
-            if (grid >= 1) kern<<<(unsigned)grid, nt, pp.smem2, st>>>(a2);
-            if (tbuf) {
-                size_t cnt = (size_t)a2.trace_sweeps * a2.trace_steps * 16;
-                std::vector<unsigned long long> h(cnt);
-                cudaMemcpyAsync(h.data(), tbuf, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
-                cudaStreamSynchronize(st);
-                if (FILE *f = fopen(tf, "wb")) {
-                    int hdr[6] = {a2.trace_sweeps, a2.trace_steps, pp.c, pp.t, pp.s, (int)grid};
-                    fwrite(hdr, sizeof(int), 6, f);
-                    fwrite(h.data(), sizeof(unsigned long long), cnt, f);
-                    fclose(f);
-                }
-                cudaFree(tbuf);
-            }
-        } else {
-            auto kern = bb::pass_flags_kernel<S>;
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem) != cudaSuccess)
-                return BB_ERR_CUDA;
-            int occ = 0;
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, pp.threads, pp.smem) != cudaSuccess)
-                return BB_ERR_CUDA;
-            if (P.cfg.max_blocks_per_sm > 0) occ = std::min(occ, (int)P.cfg.max_blocks_per_sm);
-            occ = std::max(occ, 1);
-            int64_t tasks = (int64_t)pp.nsweeps * batch;
-            int64_t grid = std::min<int64_t>(tasks, (int64_t)occ * di.sms);
-            // debug tracing (BB_TRACE_FILE, BB_TRACE_PASS): per-step timestamps of
-            // matrix 0's first sweeps in one pass, dumped after that pass
-            const char *tf = getenv("BB_TRACE_FILE");
-            const char *tp = getenv("BB_TRACE_PASS");
-            unsigned long long *tbuf = nullptr;
-            if (tf && (int)pi == (tp ? atoi(tp) : 0)) {
-                a.trace_sweeps = std::min(pp.nsweeps, 1024);
-                a.trace_steps = (int)sweep_len_h(n, pp.c, pp.t, 0);
-                size_t tb = (size_t)a.trace_sweeps * a.trace_steps * 4 * sizeof(unsigned long long);
-                if (cudaMalloc(&tbuf, tb) == cudaSuccess) {
-                    cudaMemsetAsync(tbuf, 0, tb, st);
-                    a.trace = tbuf;
-                }
-            }
-            if (grid >= 1) kern<<<(unsigned)grid, pp.threads, pp.smem, st>>>(a);
-            if (tbuf) {
-                size_t cnt = (size_t)a.trace_sweeps * a.trace_steps * 4;
-                std::vector<unsigned long long> h(cnt);
-                cudaMemcpyAsync(h.data(), tbuf, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
-                cudaStreamSynchronize(st);
-                if (FILE *f = fopen(tf, "wb")) {
-                    int hdr[6] = {a.trace_sweeps, a.trace_steps, pp.c, pp.t, pp.s, (int)grid};
-                    fwrite(hdr, sizeof(int), 6, f);
-                    fwrite(h.data(), sizeof(unsigned long long), cnt, f);
-                    fclose(f);
-                }
-                cudaFree(tbuf);
-            }
-        }
-        if (getenv("BB_DEBUG_SYNC")) { // debug: surface asynchronous kernel errors per pass
-            cudaError_t e = cudaStreamSynchronize(st);
-            if (e != cudaSuccess) {
-                fprintf(stderr, "bandbidiag: pass %d (c=%d t=%d g4=%d v2=%d) failed: %s\n", (int)pi, pp.c, pp.t,
-                        pp.g4, (int)pp.v2, cudaGetErrorString(e));
-                return BB_ERR_CUDA;
-            }
-        }
-        if (cudaGetLastError() != cudaSuccess) return BB_ERR_CUDA;
-        mark(2 + (int)pi);
-    }
-    {
-        int64_t total = (int64_t)batch * n;
-        int thr = 256;
-        int64_t blocks = std::min<int64_t>((total + thr - 1) / thr, (int64_t)di.sms * 8);
-        bb::extract_kernel<S><<<(unsigned)std::max<int64_t>(blocks, 1), thr, 0, st>>>(
-            W, mat_stride, (int)P.ldw, (int)P.ku, n, batch, reinterpret_cast<S *>(d_out), stride_d,
-            reinterpret_cast<S *>(e_out), stride_e, (P.cfg.flags & BB_FLAG_NONNEG_OUTPUT) ? 1 : 0);
-    }
-    mark(2 + (int)P.passes.size());
-    if (cudaGetLastError() != cudaSuccess) return BB_ERR_CUDA;
-    return BB_SUCCESS;
 }
 
 bb_status validate(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const void *band, int64_t ldband,
@@ -605,8 +308,9 @@ bb_status run_alloc(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const v
     return s;
 }
 
-} // namespace
+} // namespace bbhost
 
+using namespace bbhost;
 extern "C" {
 
 bb_status bb_band_to_bidiag(int64_t n, int64_t b, bb_dtype dtype, const void *band, int64_t ldband, void *d_out,

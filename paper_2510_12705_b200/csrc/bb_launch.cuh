@@ -1,0 +1,356 @@
+// bb_launch.cuh -- launch sequence of one call for storage type S: pack ->
+// one launch per pass (unit kernel v5, multi-sweep kernel v4, register
+// kernel v2 or the generic kernel, per the plan) -> extract.  Included by the
+// three per-dtype translation units so the kernels compile in parallel.
+#pragma once
+
+#include "bb_kernels.cuh"
+#include "bb_pass_v2.cuh"
+#include "bb_pass_v4.cuh"
+#include "bb_pass_v5.cuh"
+#include "bb_plan.h"
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+namespace bbhost {
+
+template <class S>
+bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t stride_band, int64_t b_in,
+                     void *d_out, int64_t stride_d, void *e_out, int64_t stride_e, void *ws, cudaStream_t st)
+{
+    DeviceInfo di;
+    if (!device_info(di)) return BB_ERR_CUDA;
+    unsigned char *base = reinterpret_cast<unsigned char *>(ws);
+    S *W = reinterpret_cast<S *>(base);
+    int *flags = reinterpret_cast<int *>(base + P.band_bytes);
+    int *counters = reinterpret_cast<int *>(base + P.band_bytes + P.flag_bytes);
+    const int64_t mat_stride = P.mat_stride;
+    const int n = (int)P.n;
+    const int batch = (int)P.batch;
+
+    cudaEvent_t *ev = reinterpret_cast<cudaEvent_t *>(P.cfg.timing_events);
+    auto mark = [&](int k) { if (ev) cudaEventRecord(ev[k], st); };
+    if (!P.passes.empty()) {
+        if (cudaMemsetAsync(flags, 0, P.flag_bytes + P.counter_bytes, st) != cudaSuccess) return BB_ERR_CUDA;
+    }
+    mark(0);
+    {
+        int64_t total = (int64_t)batch * mat_stride;
+        int thr = 256;
+        int64_t blocks = std::min<int64_t>((total + thr - 1) / thr, (int64_t)di.sms * 16);
+        bb::pack_kernel<S><<<(unsigned)std::max<int64_t>(blocks, 1), thr, 0, st>>>(
+            reinterpret_cast<const S *>(band), ldband, stride_band, (int)b_in, (int)P.b_eff, W, mat_stride,
+            (int)P.ldw, (int)P.ku, n, batch);
+    }
+    mark(1);
+    size_t npasses = P.passes.size();
+    if (const char *dp = getenv("BB_DEBUG_PASSES")) npasses = std::min(npasses, (size_t)atoi(dp)); // debug only
+    for (size_t pi = 0; pi < npasses; ++pi) {
+        const PassPlan &pp = P.passes[pi];
+        if ((int)pp.smem > di.smem_optin) return BB_ERR_NOT_SUPPORTED;
+        bb::PassArgs a{};
+        a.W = W;
+        a.mat_stride = mat_stride;
+        a.ldw = (int)P.ldw;
+        a.ku = (int)P.ku;
+        a.n = n;
+        a.c = pp.c;
+        a.t = pp.t;
+        a.s = pp.s;
+        a.batch = batch;
+        a.nsweeps = pp.nsweeps;
+        a.progress = flags + (int64_t)pi * batch * n;
+        a.counter = counters + pi;
+        a.LT = pp.LT;
+        a.LW = pp.LW;
+        if (P.cfg.schedule == BB_SCHED_CYCLE) {
+            auto kern = bb::pass_cycle_kernel<S>;
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem) != cudaSuccess)
+                return BB_ERR_CUDA;
+            int maxT = pp.cycles;
+            if (const char *dbg = getenv("BB_DEBUG_MAX_CYCLES")) maxT = std::min(maxT, atoi(dbg)); // debug only
+            for (int T = 0; T < maxT; ++T) {
+                a.cycle_T = T;
+                int rmax = std::min(T / pp.s + 1, pp.nsweeps);
+                dim3 grid((unsigned)std::max(rmax, 1), (unsigned)batch);
+                kern<<<grid, pp.threads, pp.smem, st>>>(a);
+            }
+        } else if (pp.g5 > 0) {
+            bb::PassArgsV5 a5{};
+            a5.W = W;
+            a5.mat_stride = mat_stride;
+            a5.ldw = (int)P.ldw;
+            a5.ku = (int)P.ku;
+            a5.n = n;
+            a5.c = pp.c;
+            a5.t = pp.t;
+            a5.G = pp.g5;
+            a5.a0 = pp.a5;
+            a5.b0 = pp.b5;
+            a5.batch = batch;
+            a5.nsweeps = pp.nsweeps;
+            a5.ngroups = pp.ngroups5;
+            a5.progress = a.progress;
+            a5.counter = a.counter;
+            a5.LA = pp.LA5;
+            a5.LB = pp.LB5;
+            void (*kern)(bb::PassArgsV5) = nullptr;
+            if (pp.t + 1 == 17)
+                kern = pp.g5 == 32 ? bb::pass_v5_kernel<S, 17, 8, 32>
+                                   : (pp.g5 == 16 ? bb::pass_v5_kernel<S, 17, 8, 16> : bb::pass_v5_kernel<S, 17, 8, 8>);
+            else
+                kern = pp.g5 == 32 ? bb::pass_v5_kernel<S, 33, 8, 32>
+                                   : (pp.g5 == 16 ? bb::pass_v5_kernel<S, 33, 8, 16> : bb::pass_v5_kernel<S, 33, 8, 8>);
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem5) != cudaSuccess)
+                return BB_ERR_CUDA;
+            int occ = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, pp.nt5, pp.smem5) != cudaSuccess)
+                return BB_ERR_CUDA;
+            if (occ < 1) return BB_ERR_NOT_SUPPORTED;
+            if (P.cfg.max_blocks_per_sm > 0) occ = std::min(occ, (int)P.cfg.max_blocks_per_sm);
+            const int64_t tasks = (int64_t)pp.ngroups5 * batch;
+            const int64_t grid = std::min<int64_t>(tasks, (int64_t)occ * di.sms);
+            const char *tf = getenv("BB_TRACE_FILE");
+            const char *tp = getenv("BB_TRACE_PASS");
+            unsigned long long *tbuf = nullptr;
+            if (tf && (int)pi == (tp ? atoi(tp) : 0)) {
+                a5.trace_groups = std::min(pp.ngroups5, 4096);
+                a5.trace_units = (int)sweep_len_h(n, pp.c, pp.t, 0);
+                size_t tb = (size_t)a5.trace_groups * a5.trace_units * 16 * sizeof(unsigned long long);
+                if (cudaMalloc(&tbuf, tb) == cudaSuccess) {
+                    cudaMemsetAsync(tbuf, 0, tb, st);
+                    a5.trace = tbuf;
+                }
+            }
+            if (grid >= 1) kern<<<(unsigned)grid, pp.nt5, pp.smem5, st>>>(a5);
+            if (tbuf) {
+                size_t cnt = (size_t)a5.trace_groups * a5.trace_units * 16;
+                std::vector<unsigned long long> h(cnt);
+                cudaMemcpyAsync(h.data(), tbuf, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                if (FILE *f = fopen(tf, "wb")) {
+                    int hdr[6] = {a5.trace_groups, a5.trace_units, pp.c, pp.t, pp.g5, (int)grid};
+                    fwrite(hdr, sizeof(int), 6, f);
+                    fwrite(h.data(), sizeof(unsigned long long), cnt, f);
+                    fclose(f);
+                }
+                cudaFree(tbuf);
+            }
+        } else if (pp.g4 > 0) {
+            const int G = pp.g4;
+            bb::PassArgsV4 a4{};
+            a4.W = W;
+            a4.mat_stride = mat_stride;
+            a4.ldw = (int)P.ldw;
+            a4.ku = (int)P.ku;
+            a4.n = n;
+            a4.c = pp.c;
+            a4.t = pp.t;
+            a4.a0 = pp.a4;
+            a4.b0 = pp.b4;
+            a4.batch = batch;
+            a4.nsweeps = pp.nsweeps;
+            a4.G = G;
+            a4.ngroups = (pp.nsweeps + G - 1) / G;
+            a4.progress = a.progress;
+            a4.counter = a.counter;
+            a4.NT = pp.nt4;
+            a4.LDT = pp.LDT4;
+            a4.LDW = pp.LDW4;
+            a4.NS = pp.NS4;
+            a4.slot_elems = pp.slot4;
+            a4.pw = pp.pw4;
+            int nt = G * pp.nt4 + 32 * (pp.pw4 + 1);
+            void (*kern)(bb::PassArgsV4) = nullptr;
+            constexpr bool F64 = sizeof(typename bb::ComputeOf<S>::type) == 8;
+            switch (pp.t + 1) {
+            case 16: kern = bb::pass_v4_kernel<S, 16, 576, 25>; break;
+            case 17: kern = bb::pass_v4_kernel<S, 17, 576, 25>; break;
+            case 32:
+                kern = !F64 ? bb::pass_v4_kernel<S, 32, 576, 41>
+                            : (pp.ntmax4 <= 384 ? bb::pass_v4_kernel<S, 32, 384, 35> : bb::pass_v4_kernel<S, 32, 512, 35>);
+                break;
+            default:
+                kern = !F64 ? bb::pass_v4_kernel<S, 33, 576, 41>
+                            : (pp.ntmax4 <= 384 ? bb::pass_v4_kernel<S, 33, 384, 35> : bb::pass_v4_kernel<S, 33, 512, 35>);
+                break;
+            }
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem4) != cudaSuccess)
+                return BB_ERR_CUDA;
+            int occ = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, pp.smem4) != cudaSuccess)
+                return BB_ERR_CUDA;
+            if (occ < 1) return BB_ERR_NOT_SUPPORTED;
+            if (occ >= 2 && a4.pw > 1) {
+                // several CTAs per SM (small c): resident groups bound the wavefront
+                // (each CTA holds its sweeps for ~n/c steps), so trade a producer warp
+                // for occupancy when that admits more CTAs per SM
+                int occ1 = 0;
+                const int nt1 = nt - 32 * (a4.pw - 1);
+                if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, kern, nt1, pp.smem4) == cudaSuccess &&
+                    occ1 > occ) {
+                    occ = occ1;
+                    a4.pw = 1;
+                    nt = nt1;
+                }
+            }
+            if (P.cfg.max_blocks_per_sm > 0) occ = std::min(occ, (int)P.cfg.max_blocks_per_sm);
+            else if (pp.c - pp.t == 1 && pp.c >= 32 && batch == 1) occ = 1; // measured: the sweep chain of the
+            // target-bandwidth-1 pass (c >= 32) runs faster with one CTA per SM (tools/maxb_sweep.py)
+            int64_t tasks = (int64_t)a4.ngroups * batch;
+            int64_t grid = std::min<int64_t>(tasks, (int64_t)occ * di.sms);
+            const char *tf = getenv("BB_TRACE_FILE");
+            const char *tp = getenv("BB_TRACE_PASS");
+            unsigned long long *tbuf = nullptr;
+            if (tf && (int)pi == (tp ? atoi(tp) : 0)) {
+                a4.trace_sweeps = std::min(pp.nsweeps, 1024);
+                a4.trace_steps = (int)sweep_len_h(n, pp.c, pp.t, 0);
+                size_t tb = (size_t)a4.trace_sweeps * a4.trace_steps * 16 * sizeof(unsigned long long);
+                if (cudaMalloc(&tbuf, tb) == cudaSuccess) {
+                    cudaMemsetAsync(tbuf, 0, tb, st);
+                    a4.trace = tbuf;
+                }
+            }
+            if (grid >= 1) kern<<<(unsigned)grid, nt, pp.smem4, st>>>(a4);
+            if (tbuf) {
+                size_t cnt = (size_t)a4.trace_sweeps * a4.trace_steps * 16;
+                std::vector<unsigned long long> h(cnt);
+                cudaMemcpyAsync(h.data(), tbuf, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                if (FILE *f = fopen(tf, "wb")) {
+                    int hdr[6] = {a4.trace_sweeps, a4.trace_steps, pp.c, pp.t, G, (int)grid};
+                    fwrite(hdr, sizeof(int), 6, f);
+                    fwrite(h.data(), sizeof(unsigned long long), cnt, f);
+                    fclose(f);
+                }
+                cudaFree(tbuf);
+            }
+        } else if (pp.v2) {
+            bb::PassArgsV2 a2{};
+            a2.W = W;
+            a2.mat_stride = mat_stride;
+            a2.ldw = (int)P.ldw;
+            a2.ku = (int)P.ku;
+            a2.n = n;
+            a2.c = pp.c;
+            a2.t = pp.t;
+            a2.a0 = pp.a0;
+            a2.b0 = pp.b0;
+            a2.batch = batch;
+            a2.nsweeps = pp.nsweeps;
+            a2.progress = a.progress;
+            a2.counter = a.counter;
+            a2.ntc = pp.ntc;
+            a2.LW = pp.LW2;
+            void (*kern)(bb::PassArgsV2) = nullptr;
+            const int nt = pp.ntc + 64;
+            if (nt <= 256) {
+                kern = pp.mt == 9 ? bb::pass_v2_kernel<S, 9, 256>
+                                  : (pp.mt == 17 ? bb::pass_v2_kernel<S, 17, 256> : bb::pass_v2_kernel<S, 33, 256>);
+            } else {
+                kern = pp.mt == 9 ? bb::pass_v2_kernel<S, 9, 512>
+                                  : (pp.mt == 17 ? bb::pass_v2_kernel<S, 17, 512> : bb::pass_v2_kernel<S, 33, 512>);
+            }
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem2) != cudaSuccess)
+                return BB_ERR_CUDA;
+            int occ = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, pp.smem2) != cudaSuccess)
+                return BB_ERR_CUDA;
+            if (P.cfg.max_blocks_per_sm > 0) occ = std::min(occ, (int)P.cfg.max_blocks_per_sm);
+            occ = std::max(occ, 1);
+            int64_t tasks = (int64_t)pp.nsweeps * batch;
+            int64_t grid = std::min<int64_t>(tasks, (int64_t)occ * di.sms);
+            const char *tf = getenv("BB_TRACE_FILE");
+            const char *tp = getenv("BB_TRACE_PASS");
+            unsigned long long *tbuf = nullptr;
+            if (tf && (int)pi == (tp ? atoi(tp) : 0)) {
+                a2.trace_sweeps = std::min(pp.nsweeps, 1024);
+                a2.trace_steps = (int)sweep_len_h(n, pp.c, pp.t, 0);
+                size_t tb = (size_t)a2.trace_sweeps * a2.trace_steps * 16 * sizeof(unsigned long long);
+                if (cudaMalloc(&tbuf, tb) == cudaSuccess) {
+                    cudaMemsetAsync(tbuf, 0, tb, st);
+                    a2.trace = tbuf;
+                }
+            }
+            if (grid >= 1) kern<<<(unsigned)grid, nt, pp.smem2, st>>>(a2);
+            if (tbuf) {
+                size_t cnt = (size_t)a2.trace_sweeps * a2.trace_steps * 16;
+                std::vector<unsigned long long> h(cnt);
+                cudaMemcpyAsync(h.data(), tbuf, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                if (FILE *f = fopen(tf, "wb")) {
+                    int hdr[6] = {a2.trace_sweeps, a2.trace_steps, pp.c, pp.t, pp.s, (int)grid};
+                    fwrite(hdr, sizeof(int), 6, f);
+                    fwrite(h.data(), sizeof(unsigned long long), cnt, f);
+                    fclose(f);
+                }
+                cudaFree(tbuf);
+            }
+        } else {
+            auto kern = bb::pass_flags_kernel<S>;
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem) != cudaSuccess)
+                return BB_ERR_CUDA;
+            int occ = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, pp.threads, pp.smem) != cudaSuccess)
+                return BB_ERR_CUDA;
+            if (P.cfg.max_blocks_per_sm > 0) occ = std::min(occ, (int)P.cfg.max_blocks_per_sm);
+            occ = std::max(occ, 1);
+            int64_t tasks = (int64_t)pp.nsweeps * batch;
+            int64_t grid = std::min<int64_t>(tasks, (int64_t)occ * di.sms);
+            // debug tracing (BB_TRACE_FILE, BB_TRACE_PASS): per-step timestamps of
+            // matrix 0's first sweeps in one pass, dumped after that pass
+            const char *tf = getenv("BB_TRACE_FILE");
+            const char *tp = getenv("BB_TRACE_PASS");
+            unsigned long long *tbuf = nullptr;
+            if (tf && (int)pi == (tp ? atoi(tp) : 0)) {
+                a.trace_sweeps = std::min(pp.nsweeps, 1024);
+                a.trace_steps = (int)sweep_len_h(n, pp.c, pp.t, 0);
+                size_t tb = (size_t)a.trace_sweeps * a.trace_steps * 4 * sizeof(unsigned long long);
+                if (cudaMalloc(&tbuf, tb) == cudaSuccess) {
+                    cudaMemsetAsync(tbuf, 0, tb, st);
+                    a.trace = tbuf;
+                }
+            }
+            if (grid >= 1) kern<<<(unsigned)grid, pp.threads, pp.smem, st>>>(a);
+            if (tbuf) {
+                size_t cnt = (size_t)a.trace_sweeps * a.trace_steps * 4;
+                std::vector<unsigned long long> h(cnt);
+                cudaMemcpyAsync(h.data(), tbuf, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                if (FILE *f = fopen(tf, "wb")) {
+                    int hdr[6] = {a.trace_sweeps, a.trace_steps, pp.c, pp.t, pp.s, (int)grid};
+                    fwrite(hdr, sizeof(int), 6, f);
+                    fwrite(h.data(), sizeof(unsigned long long), cnt, f);
+                    fclose(f);
+                }
+                cudaFree(tbuf);
+            }
+        }
+        if (getenv("BB_DEBUG_SYNC")) { // debug: surface asynchronous kernel errors per pass
+            cudaError_t e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) {
+                fprintf(stderr, "bandbidiag: pass %d (c=%d t=%d g4=%d v2=%d) failed: %s\n", (int)pi, pp.c, pp.t,
+                        pp.g4, (int)pp.v2, cudaGetErrorString(e));
+                return BB_ERR_CUDA;
+            }
+        }
+        if (cudaGetLastError() != cudaSuccess) return BB_ERR_CUDA;
+        mark(2 + (int)pi);
+    }
+    {
+        int64_t total = (int64_t)batch * n;
+        int thr = 256;
+        int64_t blocks = std::min<int64_t>((total + thr - 1) / thr, (int64_t)di.sms * 8);
+        bb::extract_kernel<S><<<(unsigned)std::max<int64_t>(blocks, 1), thr, 0, st>>>(
+            W, mat_stride, (int)P.ldw, (int)P.ku, n, batch, reinterpret_cast<S *>(d_out), stride_d,
+            reinterpret_cast<S *>(e_out), stride_e, (P.cfg.flags & BB_FLAG_NONNEG_OUTPUT) ? 1 : 0);
+    }
+    mark(2 + (int)P.passes.size());
+    if (cudaGetLastError() != cudaSuccess) return BB_ERR_CUDA;
+    return BB_SUCCESS;
+}
+
+
+} // namespace bbhost
