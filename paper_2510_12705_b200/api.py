@@ -56,8 +56,19 @@ class Config:
         return cfg
 
 
-def _stream() -> int:
-    return torch.cuda.current_stream().cuda_stream
+def _stream(device=None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _check_same(band: torch.Tensor, *ts):
+    """Every tensor of one call lives on band's device with band's dtype (the
+    C library launches on the current device, which the callers set to
+    band.device)."""
+    for t in ts:
+        if t.device != band.device:
+            raise ValueError(f"tensor on {t.device}, band on {band.device}")
+        if t.dtype not in (band.dtype, torch.uint8):
+            raise ValueError(f"tensor dtype {t.dtype}, band dtype {band.dtype}")
 
 
 def _cfg(cfg: Config | None, tw: int | None) -> Config:
@@ -85,10 +96,12 @@ class Workspace:
         self.n, self.b, self.batch = n, b, batch
         self.dtype = _DT_NAME[dtype] if isinstance(dtype, str) else dtype
         self.cfg = _cfg(cfg, tw)
+        dev = torch.device(device if device is not None else "cuda")
+        if dev.type == "cuda" and dev.index is None and torch.cuda.is_available():
+            dev = torch.device("cuda", torch.cuda.current_device())
         self.stats = plan(n, b, self.dtype, batch, self.cfg)
         self.nbytes = self.stats["workspace_bytes"]
-        self.buf = torch.empty(max(self.nbytes, 1), dtype=torch.uint8,
-                               device=device if device is not None else "cuda")
+        self.buf = torch.empty(max(self.nbytes, 1), dtype=torch.uint8, device=dev)
 
     def band_view(self) -> torch.Tensor:
         """Working band after a call: shape (batch, n, ldw), [k, j, ku + i - j] = A_k(i, j)."""
@@ -113,15 +126,18 @@ def band_to_bidiag(band: torch.Tensor, b: int, tw: int | None = None, cfg: Confi
     else:
         d, e = out
     c = _cfg(cfg, tw)
-    if workspace is None and c == Config():
-        N.bb_band_to_bidiag(n, b, dt, band.data_ptr(), ld, d.data_ptr(), e.data_ptr(), _stream())
-    elif workspace is None:
-        ws = Workspace(n, b, band.dtype, 1, c, device=band.device)
-        N.bb_band_to_bidiag_ex(n, b, dt, band.data_ptr(), ld, d.data_ptr(), e.data_ptr(), c.c(),
-                               ws.buf.data_ptr(), ws.nbytes, _stream())
-    else:
-        N.bb_band_to_bidiag_ex(n, b, dt, band.data_ptr(), ld, d.data_ptr(), e.data_ptr(), workspace.cfg.c(),
-                               workspace.buf.data_ptr(), workspace.nbytes, _stream())
+    _check_same(band, d, e, *([workspace.buf] if workspace is not None else []))
+    with torch.cuda.device(band.device):
+        st = _stream(band.device)
+        if workspace is None and c == Config():
+            N.bb_band_to_bidiag(n, b, dt, band.data_ptr(), ld, d.data_ptr(), e.data_ptr(), st)
+        elif workspace is None:
+            ws = Workspace(n, b, band.dtype, 1, c, device=band.device)
+            N.bb_band_to_bidiag_ex(n, b, dt, band.data_ptr(), ld, d.data_ptr(), e.data_ptr(), c.c(),
+                                   ws.buf.data_ptr(), ws.nbytes, st)
+        else:
+            N.bb_band_to_bidiag_ex(n, b, dt, band.data_ptr(), ld, d.data_ptr(), e.data_ptr(), workspace.cfg.c(),
+                                   workspace.buf.data_ptr(), workspace.nbytes, st)
     return d, e
 
 
@@ -140,8 +156,11 @@ def band_to_bidiag_batched(band: torch.Tensor, b: int, tw: int | None = None, cf
         d, e = out
     c = _cfg(cfg, tw) if workspace is None else workspace.cfg
     ws = workspace if workspace is not None else Workspace(n, b, band.dtype, B, c, device=band.device)
-    N.bb_band_to_bidiag_batched_ex(n, b, dt, B, band.data_ptr(), ld, n * ld, d.data_ptr(), d.stride(0),
-                                   e.data_ptr(), e.stride(0), c.c(), ws.buf.data_ptr(), ws.nbytes, _stream())
+    _check_same(band, d, e, ws.buf)
+    with torch.cuda.device(band.device):
+        N.bb_band_to_bidiag_batched_ex(n, b, dt, B, band.data_ptr(), ld, n * ld, d.data_ptr(), d.stride(0),
+                                       e.data_ptr(), e.stride(0), c.c(), ws.buf.data_ptr(), ws.nbytes,
+                                       _stream(band.device))
     return d, e[:, : max(n - 1, 0)]
 
 
