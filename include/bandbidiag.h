@@ -109,6 +109,9 @@ typedef enum {
                                    /* bitwise identical, for testing                     */
 #define BB_FLAG_NO_UNIT_KERNEL 0x4u /* never use the unit kernel (G sweeps advanced one step */
                                     /* at a time, bb_pass_v5.cuh); testing / comparison    */
+#define BB_FLAG_NO_SEGMENT_KERNEL 0x8u /* never use the segment-ring kernel of the target-   */
+                                       /* bandwidth-1 pass (bb_pass_v6.cuh); results are     */
+                                       /* bitwise identical, for testing / comparison        */
 
 /* Tuning knobs, the paper's hyperparameter triple.
  * Zero-initialise for defaults. */
@@ -142,8 +145,8 @@ typedef struct {
     int32_t tw;              /* resolved tilewidth                                       */
     int32_t threads_per_block;
     int64_t ldw;             /* leading dimension of the working band (elements),        */
-                             /* >= b_eff + 2 tw + 1, padded so (ldw - 1) * elem is a     */
-                             /* multiple of 16 bytes (TMA diagonal view)                  */
+                             /* >= b_eff + 2 tw + 1, padded so ldw * elem is a multiple  */
+                             /* of 16 bytes (TMA column boxes); mat_stride = n * ldw     */
     int64_t ku;              /* storage row of the diagonal in the working band          */
     int64_t mat_stride;      /* elements between consecutive matrices' working bands    */
     size_t workspace_bytes;  /* bytes bb_workspace_size() would return                   */

@@ -24,6 +24,7 @@ BB_SCHED_AUTO, BB_SCHED_FLAGS, BB_SCHED_CYCLE = 0, 1, 2
 BB_FLAG_NONNEG_OUTPUT = 0x1
 BB_FLAG_GENERIC_KERNEL = 0x2
 BB_FLAG_NO_UNIT_KERNEL = 0x4
+BB_FLAG_NO_SEGMENT_KERNEL = 0x8
 
 EXPORTED = [
     "bb_band_to_bidiag", "bb_band_to_bidiag_batched", "bb_band_to_bidiag_ex",

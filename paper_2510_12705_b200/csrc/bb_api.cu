@@ -59,13 +59,18 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
     tw = (int)std::max<int64_t>(1, std::min<int64_t>(tw, std::max<int64_t>(P.b_eff - 1, 1)));
     cfg.tw = tw;
     P.tw = tw;
-    P.ku = P.b_eff + tw;
-    P.ldw = P.b_eff + 2 * tw + 1; // band + twice the tilewidth (reading Q11)
     {
-        // TMA diagonal view: (ldw - 1) * elem must be a multiple of 16 bytes
+        // band + twice the tilewidth (reading Q11): the diagonal at storage
+        // row ku >= b_eff + tw, tw rows below it.  TMA column boxes (bb_pass_v6.cuh)
+        // need 16-byte aligned box starts and column strides: ku + 1 and ldw are
+        // rounded up to multiples of 16 / elem (the box of the last pass, c in
+        // {16, 32}, starts at row ku - (2c - 1)); a few extra zero rows at most
         const int64_t q = 16 / (int64_t)elem_size(dtype);
-        while ((P.ldw - 1) % q) ++P.ldw;
-        P.mat_stride = (n * P.ldw + q - 1) / q * q;
+        P.ku = P.b_eff + tw;
+        while ((P.ku + 1) % q) ++P.ku;
+        P.ldw = P.ku + tw + 1;
+        while (P.ldw % q) ++P.ldw;
+        P.mat_stride = n * P.ldw;
     }
     P.passes.clear();
     if (n > 2 && P.b_eff > 1) {
@@ -207,6 +212,35 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
                     pp.b5 = tight ? 4 : 5;
                     pp.nt5 = (int)std::min<int64_t>(256, std::max<int64_t>(64, (c + t + 31) / 32 * 32));
                     pp.ngroups5 = (int)((ns + pp.g5 - 1) / pp.g5);
+                }
+            }
+            // segment-ring kernel (bb_pass_v6.cuh) for target bandwidth 1: reflector
+            // length t + 1 = c in {16, 32}; G sweeps per CTA (one WG of 2c threads
+            // each); a ring of R column chunks of c columns x (3c - 1) live rows
+            // with R >= 2 + floor(1.5 (G - 1)) (WG g trails WG g-1 by 3 half-steps),
+            // plus up to 2 chunks of prefetch slack
+            if (tb == 1 && (c == 16 || c == 32) && pp.g5 == 0 && pp.s == 3 && P.ku + c + 1 <= P.ldw &&
+                !(cfg.flags & (BB_FLAG_GENERIC_KERNEL | BB_FLAG_NO_SEGMENT_KERNEL))) {
+                const int cc = (int)c;
+                const int nt = 2 * cc;
+                const int ntmax = cs == 8 ? (cc == 32 ? 384 : 448) : (cc == 32 ? 512 : 576); // bb_launch.cuh instantiations
+                int gcap = 16;
+                if (const char *e = getenv("BB_V6_G")) gcap = std::max(0, std::min(16, atoi(e)));
+                const size_t chunk = cs * (size_t)cc * (size_t)(3 * cc); // TMA box: 3c rows x c columns
+                const size_t budget = (size_t)kSmemOptinFallback - 10240; // static: barriers, counters, x staging
+                for (int G = std::min(gcap, 14); G >= 1; --G) { // named barriers 1 + g <= 15
+                    if (G * nt + 64 > ntmax) continue;
+                    const int rmin = 2 + (3 * (G - 1)) / 2;
+                    int R = 0;
+                    for (int sl = 2; sl >= 1 && !R; --sl)
+                        if ((size_t)(rmin + sl) * chunk <= budget) R = rmin + sl;
+                    if (!R) continue;
+                    pp.g6 = G;
+                    pp.r6 = R;
+                    pp.nt6 = G * nt + 64;
+                    pp.smem6 = (size_t)R * chunk + 128; // + alignment of the ring to 128 bytes
+                    pp.ngroups6 = (int)((ns + G - 1) / G);
+                    break;
                 }
             }
             P.passes.push_back(pp);

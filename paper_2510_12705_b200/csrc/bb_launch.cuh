@@ -8,13 +8,53 @@
 #include "bb_pass_v2.cuh"
 #include "bb_pass_v4.cuh"
 #include "bb_pass_v5.cuh"
+#include "bb_pass_v6.cuh"
 #include "bb_plan.h"
 
+#include <cudaTypedefs.h>
+
 #include <cstdio>
+#include <mutex>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 namespace bbhost {
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        else
+            cudaGetLastError();
+    });
+    return fn;
+}
+
+// 3-D view (ldw rows, n columns, batch matrices) of the working band, boxes of
+// box_rows x box_cols x 1 (bb_pass_v6.cuh chunk loads); false if unavailable
+template <class S>
+bool encode_band_map(CUtensorMap &map, void *W, int64_t ldw, int64_t n, int64_t batch, int box_rows, int box_cols)
+{
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    const CUtensorMapDataType dt = sizeof(S) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+                                                  : (sizeof(S) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                                                    : CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+    cuuint64_t dims[3] = {(cuuint64_t)ldw, (cuuint64_t)n, (cuuint64_t)batch};
+    cuuint64_t strides[2] = {(cuuint64_t)(ldw * sizeof(S)), (cuuint64_t)(n * ldw * sizeof(S))};
+    cuuint32_t box[3] = {(cuuint32_t)box_rows, (cuuint32_t)box_cols, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return enc(&map, dt, 3, W, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 template <class S>
 bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t stride_band, int64_t b_in,
@@ -132,6 +172,64 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
                 cudaStreamSynchronize(st);
                 if (FILE *f = fopen(tf, "wb")) {
                     int hdr[6] = {a5.trace_groups, a5.trace_units, pp.c, pp.t, pp.g5, (int)grid};
+                    fwrite(hdr, sizeof(int), 6, f);
+                    fwrite(h.data(), sizeof(unsigned long long), cnt, f);
+                    fclose(f);
+                }
+                cudaFree(tbuf);
+            }
+        } else if (pp.g6 > 0) {
+            bb::PassArgsV6 a6{};
+            a6.W = W;
+            a6.mat_stride = mat_stride;
+            a6.ldw = (int)P.ldw;
+            a6.ku = (int)P.ku;
+            a6.n = n;
+            a6.c = pp.c;
+            a6.t = pp.t;
+            a6.G = pp.g6;
+            a6.R = pp.r6;
+            a6.batch = batch;
+            a6.nsweeps = pp.nsweeps;
+            a6.ngroups = pp.ngroups6;
+            a6.progress = a.progress;
+            a6.counter = a.counter;
+            constexpr bool F64 = sizeof(typename bb::ComputeOf<S>::type) == 8;
+            CUtensorMap tmap;
+            std::memset(&tmap, 0, sizeof(tmap));
+            if (sizeof(S) != 2 && !encode_band_map<S>(tmap, W, P.ldw, n, batch, 3 * pp.c, pp.c)) return BB_ERR_CUDA;
+            void (*kern)(bb::PassArgsV6, const CUtensorMap) = nullptr;
+            if constexpr (F64) kern = pp.c == 16 ? bb::pass_v6_kernel<S, 16, 448> : bb::pass_v6_kernel<S, 32, 384>;
+            else kern = pp.c == 16 ? bb::pass_v6_kernel<S, 16, 576> : bb::pass_v6_kernel<S, 32, 512>;
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp.smem6) != cudaSuccess)
+                return BB_ERR_CUDA;
+            int occ = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, pp.nt6, pp.smem6) != cudaSuccess)
+                return BB_ERR_CUDA;
+            if (occ < 1) return BB_ERR_NOT_SUPPORTED;
+            if (P.cfg.max_blocks_per_sm > 0) occ = std::min(occ, (int)P.cfg.max_blocks_per_sm);
+            const int64_t tasks = (int64_t)pp.ngroups6 * batch;
+            const int64_t grid = std::min<int64_t>(tasks, (int64_t)occ * di.sms);
+            const char *tf = getenv("BB_TRACE_FILE");
+            const char *tp = getenv("BB_TRACE_PASS");
+            unsigned long long *tbuf = nullptr;
+            if (tf && (int)pi == (tp ? atoi(tp) : 0)) {
+                a6.trace_groups = std::min(pp.ngroups6, 4096);
+                a6.trace_steps = (int)sweep_len_h(n, pp.c, pp.t, 0) + 1;
+                size_t tb = (size_t)a6.trace_groups * a6.trace_steps * 8 * sizeof(unsigned long long);
+                if (cudaMalloc(&tbuf, tb) == cudaSuccess) {
+                    cudaMemsetAsync(tbuf, 0, tb, st);
+                    a6.trace = tbuf;
+                }
+            }
+            if (grid >= 1) kern<<<(unsigned)grid, pp.nt6, pp.smem6, st>>>(a6, tmap);
+            if (tbuf) {
+                size_t cnt = (size_t)a6.trace_groups * a6.trace_steps * 8;
+                std::vector<unsigned long long> h(cnt);
+                cudaMemcpyAsync(h.data(), tbuf, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                if (FILE *f = fopen(tf, "wb")) {
+                    int hdr[6] = {a6.trace_groups, a6.trace_steps, pp.c, pp.t, pp.g6, (int)grid};
                     fwrite(hdr, sizeof(int), 6, f);
                     fwrite(h.data(), sizeof(unsigned long long), cnt, f);
                     fclose(f);

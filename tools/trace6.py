@@ -1,0 +1,47 @@
+"""Scratch: timeline of the segment-ring kernel (bb_pass_v6.cuh) from a
+BB_TRACE_FILE dump.  Slots: 0 WG0 step j start (before its wait), 1 last WG
+step j done, 2 producer chunk j issued (after its waits), 3 writer published
+step j."""
+import sys
+import numpy as np
+
+def read(path):
+    with open(path, "rb") as f:
+        hdr = np.frombuffer(f.read(24), dtype=np.int32)
+        ng, ns, c, t, G, grid = [int(x) for x in hdr]
+        tr = np.frombuffer(f.read(), dtype=np.uint64).reshape(ng, ns, 8).astype(np.float64)
+    return (ng, ns, c, t, G, grid), tr
+
+def summarize(path):
+    (ng, ns, c, t, G, grid), tr = read(path)
+    print(f"c={c} t={t} G={G} grid={grid} groups traced={ng} steps={ns}")
+    st = tr[:, 0, 0]
+    ok = st > 0
+    idx = np.nonzero(ok)[0]
+    lags = np.diff(st[idx])
+    mid = slice(len(lags) // 4, 3 * len(lags) // 4)
+    print("  group start lag: median %.2f us mean %.2f (per sweep %.2f)" % (
+        np.median(lags[mid]) / 1e3, np.mean(lags[mid]) / 1e3, np.median(lags[mid]) / 1e3 / G))
+    k = idx[len(idx) // 2]
+    print(f"  group {k}: per step (us, relative to WG0 start of step 0)")
+    t0 = tr[k, 0, 0]
+    for j in list(range(0, 8)) + list(range(ns // 2, ns // 2 + 4)):
+        row = tr[k, j]
+        prv = tr[k - 1, j] if k > 0 else row * 0
+        print("   j=%4d wg0start %9.2f lastdone %9.2f chunk %9.2f pub %9.2f | prev pub j+1 %9.2f prev chunk %9.2f" % (
+            j, (row[0] - t0) / 1e3, (row[1] - t0) / 1e3, (row[2] - t0) / 1e3, (row[3] - t0) / 1e3,
+            (tr[k - 1, j + 1, 3] - t0) / 1e3 if k > 0 else 0, (prv[2] - t0) / 1e3))
+    # step period of WG0 and last WG in the middle of the sweep
+    s0 = np.diff(tr[k, 2:ns - 2, 0])
+    s1 = np.diff(tr[k, 2:ns - 2, 1])
+    print("  WG0 step period median %.2f us, last-WG step period %.2f us" % (np.median(s0) / 1e3, np.median(s1) / 1e3))
+    print("  last WG done(j) - WG0 start(j): median %.2f us" % (np.median(tr[k, 2:ns - 4, 1] - tr[k, 2:ns - 4, 0]) / 1e3))
+    print("  pub(j) - lastdone(j): median %.2f us" % (np.median(tr[k, 2:ns - 4, 3] - tr[k, 2:ns - 4, 1]) / 1e3))
+    print("  chunk(j) issue (next group) - pub(j+1) (this group): median %.2f us" % (
+        np.median(tr[k + 1, 2:ns - 4, 2] - tr[k, 3:ns - 3, 3]) / 1e3))
+    print("  WG0 start(j) (next group) - chunk(j) issue: median %.2f us" % (
+        np.median(tr[k + 1, 2:ns - 4, 0] - tr[k + 1, 2:ns - 4, 2]) / 1e3))
+
+if __name__ == "__main__":
+    for p in sys.argv[1:]:
+        summarize(p)
