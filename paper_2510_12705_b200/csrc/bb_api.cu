@@ -216,9 +216,7 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
             }
             // segment-ring kernel (bb_pass_v6.cuh) for target bandwidth 1: reflector
             // length t + 1 = c in {16, 32}; G sweeps per CTA (one WG of 2c threads
-            // each); a ring of R column chunks of c columns x (3c - 1) live rows
-            // with R >= 2 + floor(1.5 (G - 1)) (WG g trails WG g-1 by 3 half-steps),
-            // plus up to 2 chunks of prefetch slack
+            // each); a ring of R column chunks (c columns x 3c rows, the TMA box)
             if (tb == 1 && (c == 16 || c == 32) && pp.g5 == 0 && pp.s == 3 && P.ku + c + 1 <= P.ldw &&
                 !(cfg.flags & (BB_FLAG_GENERIC_KERNEL | BB_FLAG_NO_SEGMENT_KERNEL))) {
                 const int cc = (int)c;
@@ -230,11 +228,12 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
                 const size_t budget = (size_t)kSmemOptinFallback - 10240; // static: barriers, counters, x staging
                 for (int G = std::min(gcap, 14); G >= 1; --G) { // named barriers 1 + g <= 15
                     if (G * nt + 64 > ntmax) continue;
-                    const int rmin = 2 + (3 * (G - 1)) / 2;
-                    int R = 0;
-                    for (int sl = 2; sl >= 1 && !R; --sl)
-                        if ((size_t)(rmin + sl) * chunk <= budget) R = rmin + sl;
-                    if (!R) continue;
+                    // WG g trails WG g-1 by ~2 steps in steady state; the ring holds
+                    // the chunks from the last WG's position to WG 0's B window,
+                    // as many as shared memory allows (slack absorbs jitter)
+                    const int rmin = 3 + 2 * (G - 1);
+                    const int R = (int)std::min<size_t>(std::min<size_t>(budget / chunk, (size_t)rmin + 8), 48); // < V6_FRING
+                    if (R < rmin) continue;
                     pp.g6 = G;
                     pp.r6 = R;
                     pp.nt6 = G * nt + 64;

@@ -216,7 +216,7 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
             if (tf && (int)pi == (tp ? atoi(tp) : 0)) {
                 a6.trace_groups = std::min(pp.ngroups6, 4096);
                 a6.trace_steps = (int)sweep_len_h(n, pp.c, pp.t, 0) + 1;
-                size_t tb = (size_t)a6.trace_groups * a6.trace_steps * 8 * sizeof(unsigned long long);
+                size_t tb = (size_t)a6.trace_groups * a6.trace_steps * 16 * sizeof(unsigned long long);
                 if (cudaMalloc(&tbuf, tb) == cudaSuccess) {
                     cudaMemsetAsync(tbuf, 0, tb, st);
                     a6.trace = tbuf;
@@ -224,7 +224,7 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
             }
             if (grid >= 1) kern<<<(unsigned)grid, pp.nt6, pp.smem6, st>>>(a6, tmap);
             if (tbuf) {
-                size_t cnt = (size_t)a6.trace_groups * a6.trace_steps * 8;
+                size_t cnt = (size_t)a6.trace_groups * a6.trace_steps * 16;
                 std::vector<unsigned long long> h(cnt);
                 cudaMemcpyAsync(h.data(), tbuf, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
                 cudaStreamSynchronize(st);

@@ -180,7 +180,14 @@ __device__ __forceinline__ uint64_t *ring_slot(uint64_t *ring, int K, unsigned &
     return ring + (K % V4_RING);
 }
 
-// wait until prog[g] >= need (need >= 1 half-steps)
+// wait until prog[g] >= need (need >= 1 half-steps).  Completion of the
+// awaited event's mbarrier phase implies the counter (written before the
+// arrive) has reached `need`, so a successful try_wait ends the wait; the
+// try_wait result MUST be consumed -- otherwise the compiler drops the
+// conditional suspend and the loop spins on shared memory, stealing issue
+// slots from every working warp (ncu: 1.9e9 spin iterations in one pass).
+// A ring slot that has advanced two phases (waiter far behind) makes
+// try_wait time out; the counter re-check then ends the wait.
 __device__ __forceinline__ void wait_prog(const SyncV4 &y, int g, int need)
 {
     const int *cnt = y.prog + g;
@@ -190,7 +197,7 @@ __device__ __forceinline__ void wait_prog(const SyncV4 &y, int g, int need)
         uint64_t *b = ring_slot(((need & 1) ? y.barA : y.barS) + g * V4_RING, y.ebase[g] + k, par);
         unsigned long long t0 = 0;
         while (lds_volatile(cnt) < need) {
-            (void)mb_try_wait(b, par, 2000u);
+            if (mb_try_wait(b, par, 20000u)) break;
             if (BB_V4_WATCHDOG && !t0) t0 = gtimer();
             if (BB_V4_WATCHDOG && t0 != 1 && gtimer() - t0 > 2000000000ull) {
                 if ((threadIdx.x & 31) == 0)
@@ -303,11 +310,32 @@ template <> struct V4Math<float> {
     }
 };
 
+// Safe-range test of a sum of squares, tot in [NormRange::lo, NormRange::hi],
+// as an integer compare of the bit pattern (non-negative finite values order
+// like their bit patterns; NaN, inf and -0 fall outside): identical to the
+// floating-point test, but an integer compare is ~5 cycles on B200 where a
+// dependent fp64 compare is ~30 (tools/ubench/lat5.cu)
+template <class C> struct RangeBits;
+template <> struct RangeBits<double> {
+    static __device__ __forceinline__ bool in(double v)
+    {
+        const long long b = __double_as_longlong(v);
+        return b >= 0x05CD0B15A491EB84ll /* 1e-280 */ && b <= 0x7A11A0FC668AAC70ll /* 1e280 */;
+    }
+};
+template <> struct RangeBits<float> {
+    static __device__ __forceinline__ bool in(float v)
+    {
+        const int b = __float_as_int(v);
+        return b >= 0x15F79688 /* 1e-25f */ && b <= 0x69045951 /* 1e25f */;
+    }
+};
+
 template <class C>
 __device__ __forceinline__ bool refl_scalars(C alpha, C ssq1, C &tau, C &rho, C &beta)
 {
     const C tot = fma(alpha, alpha, ssq1);
-    if (!(tot >= NormRange<C>::lo() && tot <= NormRange<C>::hi())) return false;
+    if (!RangeBits<C>::in(tot)) return false;
     const C rn = V4Math<C>::rsq(tot);
     const C nrm = tot * rn;
     beta = alpha >= C(0) ? -nrm : nrm;
@@ -358,22 +386,28 @@ __device__ __noinline__ C refl_apply_scaled(const C *xb, int xs, int m, C *av, b
 template <class C, int MT, bool FULL, int xs>
 __device__ __forceinline__ C refl_apply(const C *xb, int m, C (&av)[MT], bool has_vec)
 {
-    bool nz = false;
     C q4[4] = {0, 0, 0, 0}, s4[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int k = 1; k < MT; ++k) {
         if (FULL || k < m) {
             const C xk = xb[k * xs];
-            nz |= (xk != C(0));
             q4[k & 3] = fma(xk, xk, q4[k & 3]);
             s4[k & 3] = fma(av[k], xk, s4[k & 3]);
         }
     }
     const C alpha = xb[0];
+    const C ssq1 = (q4[0] + q4[1]) + (q4[2] + q4[3]);
+    // identity iff x[1:] == 0 exactly (reading Q8): decided from the sum of
+    // squares (one compare instead of a chain of m dependent fp compares);
+    // only a zero sum (every square underflowed, or x[1:] == 0) looks at x
+    bool nz = ssq1 > C(0);
+    if (!nz) {
+        for (int k = 1; k < m; ++k) nz |= (xb[k * xs] != C(0));
+    }
     if (!nz) return alpha; // identity: nothing to annihilate
     C tau, rho, beta;
     asm volatile("" ::: "memory"); // re-read x below (register peak)
-    if (refl_scalars<C>(alpha, (q4[0] + q4[1]) + (q4[2] + q4[3]), tau, rho, beta)) {
+    if (refl_scalars<C>(alpha, ssq1, tau, rho, beta)) {
         if (has_vec) {
             const C w = tau * fma(rho, (s4[0] + s4[1]) + (s4[2] + s4[3]), av[0]);
             const C wr = w * rho;

@@ -52,6 +52,15 @@
 namespace bb {
 
 constexpr int V6_GMAX = 16;
+// chunk-loaded events: the producer runs up to R chunks ahead of WG 0, so the
+// ring of "chunk m loaded" mbarriers must be longer than R (a phase seen
+// twice would hang the waiter); the host caps R below this
+constexpr int V6_FRING = 64;
+__device__ __forceinline__ uint64_t *fring_slot(uint64_t *ring, int K, unsigned &par)
+{
+    par = (unsigned)(K / V6_FRING) & 1u;
+    return ring + (K % V6_FRING);
+}
 
 struct PassArgsV6 {
     void *W;
@@ -68,7 +77,7 @@ struct PassArgsV6 {
 #define TRACE6(slot_, j_)                                                                                  \
     do {                                                                                                   \
         if (a.trace && mat == 0 && k < a.trace_groups && (j_) < a.trace_steps)                            \
-            a.trace[((int64_t)k * a.trace_steps + (j_)) * 8 + (slot_)] = gtimer();                        \
+            a.trace[((int64_t)k * a.trace_steps + (j_)) * 16 + (slot_)] = gtimer();                        \
     } while (0)
 
 // ---- TMA (bulk tensor copies) ---------------------------------------------
@@ -84,6 +93,16 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, i
                  "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
                  : "memory");
 }
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, int c0, int c1, int c2, const void *src)
+{
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(su32(src))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// every bulk store of this thread complete (its writes performed)
+__device__ __forceinline__ void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 // generic-proxy accesses (flag acquire, shared-memory reads of a ring slot)
 // ordered before the async-proxy (TMA) accesses that follow
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
@@ -111,7 +130,7 @@ __device__ __forceinline__ void st_row6(C *b, int m, int kw, int wrapd, const C 
 template <class S, int MT, bool FULL, bool WRAP>
 __device__ __forceinline__ void step_v6(const PassArgsV6 &a, typename ComputeOf<S>::type *ring,
                                         typename ComputeOf<S>::type *xstage, int r0, int g, int j, int Jprev,
-                                        const SyncV4 &y, int tid, int bar, int NT)
+                                        const SyncV4 &y, int tid, int bar, int NT, unsigned long long *tr)
 {
     using C = typename ComputeOf<S>::type;
     constexpr int P = 3 * MT; // column pitch: 3c - 1 live rows (+1 pad: the TMA box)
@@ -133,13 +152,16 @@ __device__ __forceinline__ void step_v6(const PassArgsV6 &a, typename ComputeOf<
     if (warp == 0) {
         if (g == 0) {
             unsigned par;
-            uint64_t *b = ring_slot(y.barF, y.fbase + j, par); // chunk j loaded
+            uint64_t *b = fring_slot(y.barF, y.fbase + j, par); // chunk j loaded
             mb_wait(b, par);
         } else {
             wait_prog(y, g - 1, min(2 * j + 4, 2 * Jprev));
         }
     }
     nbar_sync(bar, NT);
+    if (tr && tid == 0) tr[4] = gtimer();
+#define PROBE6(i_) do { if (tr && tid == 0) tr[i_] = clock64(); } while (0)
+    PROBE6(8);
 
     // ---------------------------------------------------------------- right application (A)
     // x = A[q][p..hi]; rows q+1..hi, one per thread
@@ -162,9 +184,12 @@ __device__ __forceinline__ void step_v6(const PassArgsV6 &a, typename ComputeOf<
         }
         if constexpr (WRAP) beta1 = refl_apply<C, MT, FULL, 1>(xstage, m, av, mine);
         else beta1 = refl_apply<C, MT, FULL, P - 1>(xrow, m, av, mine);
+        PROBE6(9);
         if (mine) st_row6<S, C, MT, FULL, WRAP, P - 1>(rb, m, kw, wrapd, av);
     }
+    PROBE6(10);
     nbar_sync(bar, NT);
+    PROBE6(11);
     if (warp == 0) {
         // x row -> (beta, 0, ..., 0): exact zeros in the annihilated slots
         beta1 = StoreRound<S, C>::r(beta1);
@@ -178,7 +203,7 @@ __device__ __forceinline__ void step_v6(const PassArgsV6 &a, typename ComputeOf<
         if (g == 0) {
             if (p + c <= n - 1) { // chunk j+1 exists: loaded?
                 unsigned par;
-                uint64_t *b = ring_slot(y.barF, y.fbase + j + 1, par);
+                uint64_t *b = fring_slot(y.barF, y.fbase + j + 1, par);
                 mb_wait(b, par);
             }
         } else {
@@ -186,6 +211,8 @@ __device__ __forceinline__ void step_v6(const PassArgsV6 &a, typename ComputeOf<
         }
     }
     nbar_sync(bar, NT);
+    if (tr && tid == 0) tr[5] = gtimer();
+    PROBE6(12);
 
     // ---------------------------------------------------------------- left application (B)
     // y = A[p..hi][p], contiguous; columns p+1..ce, one per thread
@@ -204,9 +231,12 @@ __device__ __forceinline__ void step_v6(const PassArgsV6 &a, typename ComputeOf<
             for (int k = 0; k < MT; ++k) bv[k] = C(0);
         }
         beta2 = refl_apply<C, MT, FULL, 1>(ycol, m, bv, mine);
+        PROBE6(13);
         if (mine) st_vec<1, S, C, MT, FULL>(cb, m, bv);
     }
+    PROBE6(14);
     nbar_sync(bar, NT);
+    PROBE6(15);
     if (warp == 0) {
         beta2 = StoreRound<S, C>::r(beta2);
         if (lane < m) ycol[lane] = lane ? C(0) : beta2;
@@ -220,9 +250,9 @@ __device__ __forceinline__ void step_v6(const PassArgsV6 &a, typename ComputeOf<
 template <class S, int MT>
 __device__ __noinline__ void step_v6_tail(const PassArgsV6 &a, typename ComputeOf<S>::type *ring,
                                           typename ComputeOf<S>::type *xstage, int r0, int g, int j, int Jprev,
-                                          const SyncV4 &y, int tid, int bar, int NT)
+                                          const SyncV4 &y, int tid, int bar, int NT, unsigned long long *tr)
 {
-    step_v6<S, MT, false, true>(a, ring, xstage, r0, g, j, Jprev, y, tid, bar, NT);
+    step_v6<S, MT, false, true>(a, ring, xstage, r0, g, j, Jprev, y, tid, bar, NT, tr);
 }
 
 // fp16 storage: ring columns [x0, x1) loaded by one warp, widened to fp32
@@ -290,12 +320,12 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v6_kernel(PassArgsV6 a, const _
     C *ring = reinterpret_cast<C *>(smem_raw + ((128 - (su32(smem_raw) & 127)) & 127));
     __shared__ int s_task;
     __shared__ int prog_s[V6_GMAX];
-    __shared__ __align__(8) uint64_t bars[(2 * V6_GMAX + 1) * V4_RING];
+    __shared__ __align__(8) uint64_t bars[2 * V6_GMAX * V4_RING + V6_FRING];
     __shared__ int ebase_s[V6_GMAX];
     __shared__ int fbase_s;
     __shared__ volatile int wb_s; // chunks written back (ring slots free)
     __shared__ C xstage_s[V6_GMAX][MT + 1];
-    constexpr int NBAR = (2 * V6_GMAX + 1) * V4_RING;
+    constexpr int NBAR = 2 * V6_GMAX * V4_RING + V6_FRING;
 
     const int G = a.G, n = a.n, c = MT, t = MT - 1;
     const int NB = a.R * MT;
@@ -349,10 +379,14 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v6_kernel(PassArgsV6 a, const _
                     const int xb = (p - r0 - 1) % NB;
                     const bool full = p + MT - 1 <= n - 1;
                     if (g == 0 && tid == 0) TRACE6(0, j);
+                    unsigned long long *tr = (a.trace && g == 0 && mat == 0 && k < a.trace_groups && j < a.trace_steps)
+                                                 ? a.trace + ((int64_t)k * a.trace_steps + j) * 16
+                                                 : nullptr;
                     if (full && xb + MT <= NB)
-                        step_v6<S, MT, true, false>(a, ring, &xstage_s[g][0], r0, g, j, Jprev, y, tid, 1 + g, NT);
+                        step_v6<S, MT, true, false>(a, ring, &xstage_s[g][0], r0, g, j, Jprev, y, tid, 1 + g, NT, tr);
                     else
-                        step_v6_tail<S, MT>(a, ring, &xstage_s[g][0], r0, g, j, Jprev, y, tid, 1 + g, NT);
+                        step_v6_tail<S, MT>(a, ring, &xstage_s[g][0], r0, g, j, Jprev, y, tid, 1 + g, NT, tr);
+                    if (g == 0 && tid == 0) TRACE6(6, j);
                     if (g == glast && tid == 0) TRACE6(1, j);
                 }
             }
@@ -373,7 +407,7 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v6_kernel(PassArgsV6 a, const _
                 const int x0 = r0 + 1 + mm * c;
                 C *slot = ring + (size_t)(mm % a.R) * c * P;
                 unsigned par;
-                uint64_t *fb = ring_slot(y.barF, y.fbase + mm, par);
+                uint64_t *fb = fring_slot(y.barF, y.fbase + mm, par);
                 if constexpr (TMA) {
                     if (lane == 0) {
                         fence_proxy_async(); // acquired global data and freed slot -> async proxy
@@ -389,37 +423,53 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v6_kernel(PassArgsV6 a, const _
             }
         } else if ((int)threadIdx.x < ncomp + 64) {
             // ------------------------------------------------ WRITER warp: write-back + publish
+            // chunk m is final for the group once its last sweep s finished step
+            // m (every column < s + 1 + (m+1)c is); the next group's chunk m' needs
+            // our columns < r0 + G + (m'+1)c, i.e. chunk m'+1: published 2(m'+1)+2
             const int lane = threadIdx.x & 31;
             const int s = r0 + glast;
             const int Js = sweep_len(n, c, t, s);
-            const int xend = min(n, r0 + 1 + M * c);
-            int xw = r0 + 1; // next column to write back
+            auto write_chunk = [&](int mm) {
+                const int x0 = r0 + 1 + mm * c;
+                const C *slot = ring + (size_t)(mm % a.R) * c * P;
+                if constexpr (TMA) {
+                    if (lane == 0) {
+                        fence_proxy_async(); // WG writes of the slot -> async-proxy reads
+                        tma_store_3d(&tmap, ku - (2 * MT - 1), x0, mat, slot);
+                    }
+                } else {
+                    v6_store_cols<S, MT>(Wg, ku, ldw, r0, NB, x0, min(x0 + c, n), ring, lane);
+                }
+            };
+            auto publish = [&](int v, int wb) {
+                if constexpr (TMA) {
+                    if (lane == 0) tma_store_wait_all();
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    fence_proxy_async(); // async-proxy global writes -> generic release
+                    fence_acq_rel();
+                    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(gprog + k), "r"(v) : "memory");
+                    wb_s = wb;
+                }
+            };
+            int wb = 0; // chunks written back
             for (int j = 0; j < Js - 1; ++j) {
                 if (lane == 0) wait_prog(y, glast, 2 * j + 2);
                 __syncwarp();
-                const int x1 = min(s + 1 + (j + 1) * c, xend);
-                v6_store_cols<S, MT>(Wg, ku, ldw, r0, NB, xw, x1, ring, lane);
-                xw = max(xw, x1);
-                __syncwarp();
-                if (lane == 0) {
-                    fence_acq_rel();
-                    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(gprog + k), "r"(2 * j + 2) : "memory");
-                    fence_proxy_async(); // slot reads -> later TMA writes into the slot
-                    wb_s = (xw - r0 - 1) / c;
-                    TRACE6(3, j);
+                if (j < M) {
+                    write_chunk(j);
+                    wb = j + 1;
                 }
+                publish(2 * j + 2, wb);
+                if (lane == 0) TRACE6(3, j);
             }
             // every WG finished: flush the rest of the ring, publish the final value
             if (lane == 0)
                 for (int g = 0; g <= glast; ++g) wait_prog(y, g, 2 * sweep_len(n, c, t, r0 + g));
             __syncwarp();
-            v6_store_cols<S, MT>(Wg, ku, ldw, r0, NB, xw, xend, ring, lane);
-            __syncwarp();
-            if (lane == 0) {
-                fence_acq_rel();
-                asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(gprog + k), "r"(2 * Js) : "memory");
-                wb_s = M;
-            }
+            for (int mm = wb; mm < M; ++mm) write_chunk(mm);
+            publish(2 * Js, M);
         }
     }
 }

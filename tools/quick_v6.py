@@ -29,7 +29,7 @@ def small():
 if __name__ == "__main__":
     small()
     from tests.golden_util import load, errors, tol
-    for G in (2, 3, 4):
+    for G in (2, 3, 4, 5, 6):
         os.environ["BB_V6_G"] = str(G)
         print("BB_V6_G", G)
         time_cfg(32768, 128, "f64", 32)

@@ -9,7 +9,7 @@ def read(path):
     with open(path, "rb") as f:
         hdr = np.frombuffer(f.read(24), dtype=np.int32)
         ng, ns, c, t, G, grid = [int(x) for x in hdr]
-        tr = np.frombuffer(f.read(), dtype=np.uint64).reshape(ng, ns, 8).astype(np.float64)
+        tr = np.frombuffer(f.read(), dtype=np.uint64).reshape(ng, ns, 16).astype(np.float64)
     return (ng, ns, c, t, G, grid), tr
 
 def summarize(path):
@@ -34,6 +34,20 @@ def summarize(path):
     # step period of WG0 and last WG in the middle of the sweep
     s0 = np.diff(tr[k, 2:ns - 2, 0])
     s1 = np.diff(tr[k, 2:ns - 2, 1])
+    a_wait = tr[k, 2:ns - 4, 4] - tr[k, 2:ns - 4, 0]
+    a_half = tr[k, 2:ns - 4, 5] - tr[k, 2:ns - 4, 4]
+    b_half = tr[k, 2:ns - 4, 6] - tr[k, 2:ns - 4, 5]
+    print("  WG0: A wait %.2f us, A half + B wait %.2f us, B half %.2f us (medians)" % (
+        np.median(a_wait) / 1e3, np.median(a_half) / 1e3, np.median(b_half) / 1e3))
+    g0 = tr[0, 2:ns - 4]
+    print("  group 0 WG0: A wait %.2f, A+Bwait %.2f, B %.2f us" % (np.median(g0[:, 4] - g0[:, 0]) / 1e3,
+          np.median(g0[:, 5] - g0[:, 4]) / 1e3, np.median(g0[:, 6] - g0[:, 5]) / 1e3))
+    cy = tr[k, 2:ns - 4]
+    names = ["A: loads+dot+scalars+update (refl_apply)", "A: store row", "A: barrier", "B: ...refl_apply", "B: store col", "B: barrier"]
+    pairs = [(8, 9), (9, 10), (10, 11), (12, 13), (13, 14), (14, 15)]
+    for nm, (a0, a1) in zip(names, pairs):
+        print("  cycles %-42s %7.0f" % (nm, np.median(cy[:, a1] - cy[:, a0])))
+    print("  cycles A-post..B-start (incl. B wait) %7.0f" % np.median(cy[:, 12] - cy[:, 11]))
     print("  WG0 step period median %.2f us, last-WG step period %.2f us" % (np.median(s0) / 1e3, np.median(s1) / 1e3))
     print("  last WG done(j) - WG0 start(j): median %.2f us" % (np.median(tr[k, 2:ns - 4, 1] - tr[k, 2:ns - 4, 0]) / 1e3))
     print("  pub(j) - lastdone(j): median %.2f us" % (np.median(tr[k, 2:ns - 4, 3] - tr[k, 2:ns - 4, 1]) / 1e3))
