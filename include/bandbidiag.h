@@ -183,8 +183,11 @@ bb_status bb_band_to_bidiag_batched_ex(int64_t n, int64_t b, bb_dtype dtype, int
 
 /* End-to-end form with HOST buffers (pageable or pinned): copies the bands
  * host->device, reduces, copies d, e device->host, all on `stream`, and
- * BLOCKS until d_out/e_out are valid on the host.  Device memory is
- * allocated stream-ordered per call. */
+ * BLOCKS until d_out/e_out are valid on the host.  Device memory: one
+ * staging buffer per device (band copy, d, e, workspace), allocated on first
+ * use, grown when a larger call needs it, kept until process exit; host
+ * calls serialise on it (a mutex), so concurrent calls are safe but not
+ * concurrent. */
 bb_status bb_band_to_bidiag_host(int64_t n, int64_t b, bb_dtype dtype, int64_t batch,
                                  const void *band_host, int64_t ldband, int64_t stride_band,
                                  void *d_host, int64_t stride_d, void *e_host, int64_t stride_e,

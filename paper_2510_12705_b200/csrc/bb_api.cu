@@ -398,13 +398,33 @@ bb_status bb_band_to_bidiag_host(int64_t n, int64_t b, bb_dtype dtype, int64_t b
     const size_t band_b = align_up((size_t)batch * stride_band * es);
     const size_t d_b = align_up((size_t)batch * stride_d * es);
     const size_t e_b = align_up((size_t)batch * std::max<int64_t>(stride_e, 1) * es);
-    unsigned char *buf = nullptr;
     const size_t total = band_b + d_b + e_b + P.total;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&buf), total, st);
-    if (e != cudaSuccess) {
+    // per-device staging buffer, kept between calls (grown on demand) so the
+    // host path does not pay an allocation per call; calls serialise on it
+    static std::mutex mu;
+    static std::vector<std::pair<void *, size_t>> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
         cudaGetLastError();
-        return e == cudaErrorMemoryAllocation ? BB_ERR_OUT_OF_MEMORY : BB_ERR_CUDA;
+        return BB_ERR_CUDA;
     }
+    if ((int)cache.size() <= dev) cache.resize(dev + 1, {nullptr, 0});
+    if (cache[dev].second < total) {
+        if (cache[dev].first) {
+            if (cudaStreamSynchronize(st) != cudaSuccess) return BB_ERR_CUDA;
+            cudaFree(cache[dev].first);
+            cache[dev] = {nullptr, 0};
+        }
+        void *p = nullptr;
+        cudaError_t e = cudaMalloc(&p, total);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return e == cudaErrorMemoryAllocation ? BB_ERR_OUT_OF_MEMORY : BB_ERR_CUDA;
+        }
+        cache[dev] = {p, total};
+    }
+    unsigned char *buf = reinterpret_cast<unsigned char *>(cache[dev].first);
     void *dband = buf, *dd = buf + band_b, *de = buf + band_b + d_b, *ws = buf + band_b + d_b + e_b;
     const size_t in_bytes = (size_t)((batch - 1) * stride_band + n * ldband) * es;
     if (cudaMemcpyAsync(dband, band_host, in_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) s = BB_ERR_CUDA;
@@ -418,7 +438,6 @@ bb_status bb_band_to_bidiag_host(int64_t n, int64_t b, bb_dtype dtype, int64_t b
             if (cudaMemcpyAsync(e_host, de, en, cudaMemcpyDeviceToHost, st) != cudaSuccess) s = BB_ERR_CUDA;
         }
     }
-    if (cudaFreeAsync(buf, st) != cudaSuccess && s == BB_SUCCESS) s = BB_ERR_CUDA;
     if (cudaStreamSynchronize(st) != cudaSuccess && s == BB_SUCCESS) s = BB_ERR_CUDA;
     return s;
 }
@@ -451,18 +470,35 @@ bb_status bb_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const bb_
     int64_t steps = 0, crit = 0;
     for (const PassPlan &pp : P.passes) {
         crit += pp.cycles;
+        const int64_t c = pp.c, t = pp.t;
+        auto one = [&](int64_t r, int64_t j) {
+            int64_t p = r + (c - t) + j * c;
+            int64_t q = j ? p - c : r;
+            int64_t hi = std::min<int64_t>(p + t, n - 1);
+            int64_t ce = std::min<int64_t>(hi + c, n - 1);
+            int64_t m = hi - p + 1;
+            elems += (double)(m * ((hi - q + 1) + (ce - p + 1) - m));
+            flops += (double)(4 * m * (hi - q) + 4 * m * (ce - p) + 6 * m);
+        };
+        // interior steps (j >= 1, window unclipped: p + t + c <= n - 1) all move
+        // (t+1)(2c+t+1) elements and 8(t+1)(c+t) + 6(t+1) flops; the first step
+        // and the clipped tail of each sweep are counted one by one
+        const double e_int = (double)((t + 1) * (2 * c + t + 1));
+        const double f_int = (double)(8 * (t + 1) * (c + t) + 6 * (t + 1));
         for (int64_t r = 0; r < pp.nsweeps; ++r) {
-            int64_t J = sweep_len_h(n, pp.c, pp.t, r);
-            for (int64_t j = 0; j < J; ++j) {
-                int64_t p = r + (pp.c - pp.t) + j * pp.c;
-                int64_t q = j ? p - pp.c : r;
-                int64_t hi = std::min<int64_t>(p + pp.t, n - 1);
-                int64_t ce = std::min<int64_t>(hi + pp.c, n - 1);
-                int64_t m = hi - p + 1;
-                elems += (double)(m * ((hi - q + 1) + (ce - p + 1) - m));
-                flops += (double)(4 * m * (hi - q) + 4 * m * (ce - p) + 6 * m);
-                ++steps;
+            const int64_t J = sweep_len_h(n, c, t, r);
+            steps += J;
+            if (J == 0) continue;
+            one(r, 0);
+            // last j with r + (c - t) + j c + t + c <= n - 1
+            const int64_t num = n - 1 - r - 2 * c;
+            int64_t jint = num >= 0 ? num / c : 0;
+            jint = std::min<int64_t>(jint, J - 1);
+            if (jint >= 1) {
+                elems += e_int * (double)jint;
+                flops += f_int * (double)jint;
             }
+            for (int64_t j = std::max<int64_t>(1, jint + 1); j < J; ++j) one(r, j);
         }
     }
     out->steps = steps;

@@ -107,11 +107,13 @@ def test_plan_matches_oracle_enumeration(n, b, dt, tw, es):
     assert st["alg_bytes"] == w["bytes"]
     assert st["alg_flops"] == w["flops"]
     beff = min(b, n - 1)
-    assert st["ldw"] >= beff + 2 * st["tw"] + 1      # band + 2 tw headroom
-    assert st["ldw"] <= beff + 2 * st["tw"] + 1 + 16 // es
-    assert ((st["ldw"] - 1) * es) % 16 == 0          # TMA diagonal-view stride
-    assert (st["mat_stride"] * es) % 16 == 0 and st["mat_stride"] >= n * st["ldw"]
-    assert st["ku"] == beff + st["tw"]
+    q = 16 // es
+    # band + 2 tw headroom: diagonal at row ku >= beff + tw, tw rows below
+    assert beff + st["tw"] <= st["ku"] < beff + st["tw"] + q
+    assert ((st["ku"] + 1) * es) % 16 == 0           # TMA box start of the last pass
+    assert st["ku"] + st["tw"] + 1 <= st["ldw"] < st["ku"] + st["tw"] + 1 + q
+    assert (st["ldw"] * es) % 16 == 0                # TMA column stride
+    assert st["mat_stride"] == n * st["ldw"]
 
 
 def test_default_tilewidth_per_dtype():
