@@ -2,18 +2,34 @@
 """bench.py -- band -> bidiagonal reduction on B200 (arXiv 2510.12705 hot path).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload single|batched] [--dtype f64|f32|f16] [--n N] [--b B] [--tw TW]
+                    [--dtype f64|f32|f16] [--n N] [--b B] [--tw TW]
+                    [--no-extra] [--no-batched] [--no-cpu-baseline] [--no-e2e]
+                    [--backend nccl|gloo] [--dry-run]
 
-A "step" is one full reduction (every pass of Alg. 1, pack + passes +
-extract) of one batch of synthetic banded matrices.  Default workload
-(N=1): BASELINE config 4, one n=32768, b=128 matrix per GPU (fp64, tw=16),
-i.i.d. N(0,1) band entries.  --workload batched: BASELINE config 5, 64
-matrices n=16384 split across the ranks (strong scaling).  Under torchrun,
-the single workload gives each rank its own matrix (weak scaling) and the
-results are gathered with NCCL (the only collective).
+A "step" is one full reduction (pack + every pass of Alg. 1 + extract) of
+one batch of synthetic banded matrices, inputs resident in HBM.
 
-Metric (BASELINE.json): effective GB/s = algorithmic bytes (SURVEY §8d:
-each step's two-sided window read once + written once) / device time; also
+Top-level line (the driver's number): BASELINE config 4 -- one n=32768,
+b=128 matrix per GPU (fp64, tw=32), i.i.d. N(0,1) band entries.  At N > 1
+every rank reduces its own matrix (weak scaling; one matrix never spans GPUs,
+its sweeps are a strict chain -- DESIGN.md section 9).  `value` = algorithmic
+bytes of all ranks / max-over-ranks device time.
+
+Sub-records in the same line:
+  "batched": BASELINE config 5 -- 64 matrices n=16384, b=128, fp64 split
+             across the N ranks (strong scaling), matrices/s, per-GPU GB/s, the
+             NCCL all-gather of (d, e) timed separately, parity of matrices
+             0 / 63 against the oracle's golden files;
+  "extra":   (N = 1) config 4 in fp32, config 2 (n=1024), config 3 (n=8192),
+             each with its own roofline fraction;
+  "parity":  the timed output itself against tests/golden/ (oracle-written).
+
+--gpus N without torchrun re-launches itself under torch.distributed.run
+(one rank per GPU, 127.0.0.1 rendezvous).  --dry-run (CPU, gloo) exercises
+spawn, the all-gather and the JSON line without any device work.
+
+Metric (BASELINE.json): effective GB/s = algorithmic bytes (each
+step's two-sided window read once + written once) / device time; also
 GFLOP/s and matrices/s.  Roofline: the pass kernels' algorithmic bytes over
 their CUDA-event time vs the measured HBM copy bandwidth.
 """
@@ -22,7 +38,9 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -33,54 +51,56 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 ES = {"f16": 2, "f32": 4, "f64": 8}
-DEFAULT_TW = {"f16": 32, "f32": 32, "f64": 32}
+METRIC = "band_to_bidiag_effective_GBps"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="single", choices=["single", "batched"])
     ap.add_argument("--dtype", default="f64", choices=["f16", "f32", "f64"])
-    ap.add_argument("--n", type=int, default=0)
-    ap.add_argument("--b", type=int, default=0)
-    ap.add_argument("--tw", type=int, default=0)
-    ap.add_argument("--batch", type=int, default=0, help="batched workload: total matrices (default 64)")
-    ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--b", type=int, default=128)
+    ap.add_argument("--tw", type=int, default=32)
     ap.add_argument("--maxb", type=int, default=0)
+    ap.add_argument("--batch", type=int, default=64, help="batched sub-record: total matrices")
+    ap.add_argument("--batched-n", type=int, default=16384)
+    ap.add_argument("--batched-b", type=int, default=128)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="cpu_baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--no-batched", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--dry-run", action="store_true", help="no device work: spawn + gather + JSON only")
     ap.add_argument("--seed", type=int, default=0)
-    a = ap.parse_args()
-    if a.workload == "single":
-        a.n = a.n or 32768
-        a.b = a.b or 128
-    else:
-        a.n = a.n or 16384
-        a.b = a.b or 128
-        a.batch = a.batch or 64
-    a.tw = a.tw or DEFAULT_TW[a.dtype]
-    return a
+    return ap.parse_args(argv)
 
 
-# --------------------------------------------------------------------------- dist
+# --------------------------------------------------------------------------- ranks
 def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def matrices_for_rank(a, world, rank):
-    """Global matrix ids this rank reduces."""
-    from paper_2510_12705_b200.dist import partition
-    if a.workload == "single":
-        return [rank]                      # weak scaling: one n x n matrix per GPU
-    start, count = partition(a.batch, world, rank)
-    return list(range(start, start + count))
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch_if_needed(a):
+    """--gpus N without a torchrun environment: re-exec under torch.distributed.run,
+    one process per GPU; returns the child's exit code (None: run here)."""
+    if a.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # --------------------------------------------------------------------------- clocks
@@ -106,8 +126,7 @@ class ClockSampler:
     def _reason_names(self, mask):
         nv = self.nv
         names = []
-        table = [("gpu_idle", "nvmlClocksThrottleReasonGpuIdle"),
-                 ("applications_clocks_setting", "nvmlClocksThrottleReasonApplicationsClocksSetting"),
+        table = [("applications_clocks_setting", "nvmlClocksThrottleReasonApplicationsClocksSetting"),
                  ("sw_power_cap", "nvmlClocksThrottleReasonSwPowerCap"),
                  ("hw_slowdown", "nvmlClocksThrottleReasonHwSlowdown"),
                  ("sync_boost", "nvmlClocksThrottleReasonSyncBoost"),
@@ -126,9 +145,7 @@ class ClockSampler:
                 mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
                 mask = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
                 self.samples.append(mhz)
-                for r in self._reason_names(mask):
-                    if r != "gpu_idle":
-                        self.reasons.add(r)
+                self.reasons.update(self._reason_names(mask))
             except Exception:
                 pass
             time.sleep(0.1)
@@ -147,26 +164,49 @@ class ClockSampler:
                 "samples": len(self.samples), "source": "nvml" if self.ok else "unavailable"}
 
 
-# --------------------------------------------------------------------------- peaks
+# --------------------------------------------------------------------------- peaks, host
 def hbm_peak():
-    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
-        with open(p) as f:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
 def ncu_traffic(key):
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    """DRAM bytes (read + write) per step of the pass kernels, summed over the
+    pass launches, from this round's ncu capture (profiles/ncu_traffic.json,
+    written by tools/ncu_traffic.py from an ncu CSV); None if not measured."""
     try:
-        with open(p) as f:
-            return json.load(f).get(key)
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            v = json.load(f).get(key)
+        return v
     except Exception:
         return None
 
 
+def host_info():
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
 # --------------------------------------------------------------------------- CPU oracle
+def _oracle_native_once():
+    import oracle
+    if not getattr(_oracle_native_once, "done", False):
+        _oracle_native_once.flags = oracle.use_native_build("/tmp/bb_oracle_native") or \
+            "-O2 -ffp-contract=off (portable build)"
+        _oracle_native_once.done = True
+    return _oracle_native_once.flags
+
+
 def oracle_sample(band, b, tw, dtype, budget_s):
     """Time the CPU oracle (as it stands, single thread) on a bounded sample of
     the workload: the first S steps of the sequential reduction of one matrix,
@@ -189,6 +229,31 @@ def oracle_sample(band, b, tw, dtype, budget_s):
             "gbs": bytes_ / dt / 1e9, "sample": f"first {done} steps (sequential order, pass 1) of matrix 0"}
 
 
+def _batched_cpu_worker(args):
+    n, b, tw, mid, budget = args
+    import synth
+    _oracle_native_once()
+    band = synth.random_band(n, b, "f64", seed=0, matrix_id=mid)
+    return oracle_sample(band, b, tw, "f64", budget)
+
+
+def batched_cpu(n, b, tw, mat_bytes, budget):
+    """P = min(64, cores) oracle processes at once, one matrix each, a bounded
+    sample per process; host matrices/s = P / (per-matrix bytes / per-process rate)."""
+    from multiprocessing import get_context
+    P = max(1, min(64, os.cpu_count() or 1))
+    t0 = time.perf_counter()
+    with get_context("spawn").Pool(P) as pool:
+        res = pool.map(_batched_cpu_worker, [(n, b, tw, m, budget) for m in range(P)])
+    wall = time.perf_counter() - t0
+    rate = sum(r["alg_bytes"] for r in res) / max(r["seconds"] for r in res)  # B/s, all processes
+    return {"value": mat_bytes and rate / mat_bytes, "unit": "matrices/s", "gbs": rate / 1e9, "processes": P,
+            "cores": P, "kind": "oracle",
+            "sample": f"{P} concurrent oracle processes, each the first ~{budget:.0f} s of steps of one "
+                      f"n={n} b={b} fp64 matrix; matrices/s = aggregate bytes/s / bytes per matrix",
+            "wall_s": wall}
+
+
 def run_reference(a):
     """--impl reference: the CPU oracle on the host cores (the base contract's
     reference arm for this tier), same config/metric/unit."""
@@ -196,12 +261,11 @@ def run_reference(a):
     if rank != 0:
         return
     import synth
+    flags = _oracle_native_once()
     band = synth.random_band(a.n, a.b, a.dtype, seed=a.seed, matrix_id=0)
     for _ in range(a.warmup):
         oracle_sample(band, a.b, a.tw, a.dtype, 0.5)
-    vals = []
-    tsum = 0.0
-    last = None
+    vals, tsum, last = [], 0.0, None
     per = max(1.0, min(a.cpu_seconds, 60.0) / max(a.steps, 1))
     for _ in range(a.steps):
         r = oracle_sample(band, a.b, a.tw, a.dtype, per)
@@ -209,177 +273,319 @@ def run_reference(a):
         tsum += r["seconds"]
         last = r
     v = float(np.mean(vals))
-    out = {"impl": "reference", "metric": "band_to_bidiag_effective_GBps", "value": v, "unit": "GB/s",
-           "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * tsum / a.steps,
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s",
+           "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * tsum / a.steps,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": a.dtype,
            "data": "synthetic: i.i.d. N(0,1) band entries (numpy Philox, seed %d)" % a.seed,
-           "config": workload_config(a),
-           "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": last["sample"]},
+           "config": workload_config(a, world),
+           "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": last["sample"],
+                            "build": flags, "host": host_info()},
            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
-def workload_config(a):
-    if a.workload == "single":
-        w = f"single n={a.n} b={a.b} {a.dtype} tw={a.tw} (BASELINE config 4)"
-    else:
-        w = f"batched {a.batch} x n={a.n} b={a.b} {a.dtype} tw={a.tw} (BASELINE config 5)"
-    return {"workload": w, "n": a.n, "b": a.b, "tw": a.tw, "batch": (a.batch if a.workload == "batched" else None),
-            "parallelism": f"dp{a.gpus}", "l2": "flushed between timed steps (256 MiB write); "
-            "within a step the working band is L2-resident by design"}
+def workload_config(a, world):
+    return {"workload": f"single n={a.n} b={a.b} {a.dtype} tw={a.tw} per GPU (BASELINE config 4)",
+            "n": a.n, "b": a.b, "tw": a.tw, "matrices_per_gpu": 1, "parallelism": f"dp{world}",
+            "l2": "flushed between timed steps (256 MiB write); within a step the working band is "
+                  "L2-resident by design"}
 
 
-# --------------------------------------------------------------------------- ours
+# --------------------------------------------------------------------------- device helpers
+class Runner:
+    """One configuration on this rank's device: inputs generated once (seeded,
+    matrix ids), copied to HBM, a pre-allocated workspace, per-pass CUDA events."""
+
+    def __init__(self, bb, torch, dev, n, b, dtype, tw, ids, maxb=0, seed=0):
+        import synth
+        self.bb, self.torch, self.dev = bb, torch, dev
+        self.n, self.b, self.dtype, self.tw, self.ids = n, b, dtype, tw, ids
+        self.B = len(ids)
+        self.host = np.stack([synth.random_band(n, b, dtype, seed=seed, matrix_id=i) for i in ids])
+        self.band = torch.from_numpy(self.host).to(dev)
+        self.cfg = bb.Config(tw=tw, max_blocks_per_sm=maxb)
+        self.ws = bb.Workspace(n, b, dtype, self.B, cfg=self.cfg, device=dev)
+        self.st = self.ws.stats
+        self.P = self.st["passes"]
+        self.d = torch.empty(self.B, n, dtype=self.band.dtype, device=dev)
+        self.e = torch.empty(self.B, max(n - 1, 1), dtype=self.band.dtype, device=dev)
+        self.stream = torch.cuda.current_stream(dev)
+        self.launches = bb.launch_count(n, b, dtype, self.B, self.cfg)
+
+    def step(self, events=None):
+        bb = self.bb
+        c = bb.Config(**{**self.cfg.__dict__, "timing_events": tuple(events) if events else ()})
+        bb.bb_band_to_bidiag_batched_ex(self.n, self.b, bb.api.bb_dtype(self.dtype), self.B, self.band.data_ptr(),
+                                        self.b + 1, self.n * (self.b + 1), self.d.data_ptr(), self.d.stride(0),
+                                        self.e.data_ptr(), self.e.stride(0), c.c(), self.ws.buf.data_ptr(),
+                                        self.ws.nbytes, self.stream.cuda_stream)
+
+    def timed(self, steps, warmup, flush, barrier=lambda: None):
+        torch = self.torch
+        for _ in range(warmup):
+            flush.fill_(1.0)
+            self.step()
+        torch.cuda.synchronize()
+        step_ms, pass_ms = [], []
+        barrier()
+        torch.cuda.synchronize()
+        for _ in range(steps):
+            flush.fill_(1.0)                        # evict L2 between timed steps
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(self.P + 3)]
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(self.stream)
+            self.step(evs)
+            s1.record(self.stream)
+            torch.cuda.synchronize()
+            step_ms.append(s0.elapsed_time(s1))
+            pass_ms.append([evs[1 + p].elapsed_time(evs[2 + p]) for p in range(self.P)])
+        torch.cuda.synchronize()
+        barrier()
+        return step_ms, pass_ms
+
+    def roofline(self, pass_ms, ms_per_step):
+        peak, src = hbm_peak()
+        pm = np.mean(np.array(pass_ms), axis=0) if len(pass_ms) else np.zeros(self.P)
+        tot = float(np.sum(pm))
+        ach = self.st["alg_bytes"] * self.B / (tot * 1e-3) / 1e9 if tot > 0 else None
+        key = f"{self.n}:{self.b}:{self.dtype}:{self.tw}:{self.B}"
+        tr = ncu_traffic(key)
+        return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": (ach / peak) if ach else None, "traffic": tr,
+                "traffic_source": ("profiles/ncu_traffic.json[%s] (ncu dram__bytes_read+write, pass kernels, "
+                                   "per step)" % key) if tr is not None else None,
+                "peak_source": src,
+                "kernel": "pass kernels: pass_v5_kernel (unit kernel, target bandwidth >= 8), pass_v6_kernel "
+                          "(segment ring, target bandwidth 1)",
+                "alg_bytes_per_step": self.st["alg_bytes"] * self.B,
+                "pass_ms_mean": [float(x) for x in pm],
+                "pass_share_of_step": tot / ms_per_step if ms_per_step else None}
+
+    def parity(self, golden_names):
+        """The timed output against oracle-written golden files (|d|, |e|,
+        normwise, north_star tolerances, reading Q15)."""
+        from tests.golden_util import errors, golden_path, input_sha256, load, tol
+        d = self.d.double().cpu().numpy()
+        e = self.e[:, : self.n - 1].double().cpu().numpy()
+        out = []
+        for k, name in golden_names:
+            if not os.path.exists(golden_path(name)):
+                continue
+            g = load(name)
+            same_input = input_sha256(self.host[k]) == g["sha256"]
+            err = errors(g, d[k], e[k])
+            lim = tol(self.dtype, self.n)
+            rel = max(err["d"], err["e"]) / g["fro"]
+            out.append({"golden": name, "same_input": same_input, "max_abs_err_over_normF": rel, "tol": lim,
+                        "ok": bool(same_input and rel <= lim)})
+        return out
+
+
+def record(r, step_ms, pass_ms, mats_total, ms=None, label=""):
+    ms = ms if ms is not None else float(np.mean(step_ms))
+    ab = r.st["alg_bytes"] * mats_total
+    return {"workload": label, "n": r.n, "b": r.b, "dtype": r.dtype, "tw": r.tw, "matrices": mats_total,
+            "ms_per_step": ms, "value": ab / (ms * 1e-3) / 1e9, "unit": "GB/s",
+            "gflops": r.st["alg_flops"] * mats_total / (ms * 1e-3) / 1e9, "matrices_per_s": mats_total / (ms * 1e-3),
+            "roofline": r.roofline(pass_ms, ms)}
+
+
+# --------------------------------------------------------------------------- main
 def main():
     a = parse()
+    rc = relaunch_if_needed(a)
+    if rc is not None:
+        sys.exit(rc)
     if a.impl == "reference":
         run_reference(a)
         return
     import torch
     import torch.distributed as dist
-
-    import synth
-    import paper_2510_12705_b200 as bb
-    from paper_2510_12705_b200.dist import gather_results
+    from paper_2510_12705_b200.dist import gather_results, partition
 
     world, rank, local = dist_env()
+    if a.dry_run:
+        return dry_run(a, world, rank)
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group(a.backend, device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
-    stream = torch.cuda.current_stream()
+    import paper_2510_12705_b200 as bb
+    barrier = (lambda: dist.barrier()) if world > 1 else (lambda: None)
 
-    ids = matrices_for_rank(a, world, rank)
-    B = len(ids)
-    bands_np = np.stack([synth.random_band(a.n, a.b, a.dtype, seed=a.seed, matrix_id=i) for i in ids])
-    band = torch.from_numpy(bands_np).to(dev)
-    cfg = bb.Config(tw=a.tw, threads_per_block=a.threads, max_blocks_per_sm=a.maxb)
-    ws = bb.Workspace(a.n, a.b, a.dtype, B, cfg=cfg, device=dev)
-    st = ws.stats
-    P = st["passes"]
-    d = torch.empty(B, a.n, dtype=band.dtype, device=dev)
-    e = torch.empty(B, max(a.n - 1, 1), dtype=band.dtype, device=dev)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    launches_per_step = bb.launch_count(a.n, a.b, a.dtype, B, cfg)
-
-    def step(events=None):
-        c = bb.Config(**{**cfg.__dict__, "timing_events": tuple(events) if events else ()})
-        bb.bb_band_to_bidiag_batched_ex(a.n, a.b, bb.api.bb_dtype(a.dtype), B, band.data_ptr(), a.b + 1,
-                                        a.n * (a.b + 1), d.data_ptr(), d.stride(0), e.data_ptr(), e.stride(0),
-                                        c.c(), ws.buf.data_ptr(), ws.nbytes, stream.cuda_stream)
-        if world > 1:
-            gather_results(d, e, world)
-
-    for _ in range(a.warmup):
-        flush.fill_(1.0)
-        step()
-    torch.cuda.synchronize()
-
-    clocks = ClockSampler(dev.index)
-    step_ms = []
-    pass_ms = []
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks.start()
-    for _ in range(a.steps):
-        flush.fill_(1.0)                         # evict L2 between timed steps
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(P + 3)]
-        s0 = torch.cuda.Event(enable_timing=True)
-        s1 = torch.cuda.Event(enable_timing=True)
-        s0.record(stream)
-        step(evs)
-        s1.record(stream)
-        torch.cuda.synchronize()
-        step_ms.append(s0.elapsed_time(s1))
-        pass_ms.append([evs[1 + p].elapsed_time(evs[2 + p]) for p in range(P)])
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clk = clocks.stop()
-
-    total_ms = float(sum(step_ms))
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / a.steps
-    mats_total = a.batch if a.workload == "batched" else world
-    alg_bytes_step = st["alg_bytes"] * mats_total          # all ranks
-    alg_flops_step = st["alg_flops"] * mats_total
+        return float(t.item())
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    # ---------------------------------------------------------------- headline: config 4, one matrix per GPU
+    head = Runner(bb, torch, dev, a.n, a.b, a.dtype, a.tw, [rank], maxb=a.maxb, seed=a.seed)
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    step_ms, pass_ms = head.timed(a.steps, a.warmup, flush, barrier)
+    clk = clocks.stop()
+    ms_per_step = max_over_ranks(float(np.mean(step_ms)))
+    alg_bytes_step = head.st["alg_bytes"] * world
     value = alg_bytes_step / (ms_per_step * 1e-3) / 1e9
-    gflops = alg_flops_step / (ms_per_step * 1e-3) / 1e9
-    mps = mats_total / (ms_per_step * 1e-3)
+    gname = f"c4_n{a.n}_b{a.b}_{a.dtype}_s{a.seed}_m{rank}"
+    parity = head.parity([(0, gname)])
 
-    # roofline of the dominant kernel (the per-pass persistent kernels), this rank
-    pass_total_ms = float(np.sum(pass_ms)) / a.steps
-    achieved = st["alg_bytes"] * B / (pass_total_ms * 1e-3) / 1e9
-    peak, peak_src = hbm_peak()
-    key = f"{a.workload}:{a.n}:{a.b}:{a.dtype}:{a.tw}"
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": ncu_traffic(key), "peak_source": peak_src,
-            "kernel": "pass_v4_kernel (multi-sweep persistent launch per pass; v2 register kernel where v4 does not apply)",
-            "alg_bytes_per_step_per_rank": st["alg_bytes"] * B,
-            "pass_ms_mean": [float(x) for x in np.mean(np.array(pass_ms), axis=0)],
-            "pass_share_of_step": pass_total_ms / ms_per_step}
-
-    # parity spot check of this run's output (cheap, always on): structural invariants
-    torch.cuda.synchronize()
-
-    # e2e: the C-ABI host entry point, host buffers, H2D + D2H inside the region
+    # e2e: the C-ABI host entry point, pinned host buffers, H2D + D2H inside the region
     e2e = None
     if not a.no_e2e:
-        pin = torch.from_numpy(bands_np).pin_memory()
-        dh = torch.empty(B, a.n, dtype=pin.dtype).pin_memory()
-        eh = torch.empty(B, max(a.n - 1, 1), dtype=pin.dtype).pin_memory()
+        pin = torch.from_numpy(head.host).pin_memory()
+        dh = torch.empty(1, a.n, dtype=pin.dtype).pin_memory()
+        eh = torch.empty(1, max(a.n - 1, 1), dtype=pin.dtype).pin_memory()
 
         def e2e_step():
-            bb.bb_band_to_bidiag_host(a.n, a.b, bb.api.bb_dtype(a.dtype), B, pin.data_ptr(), a.b + 1,
+            bb.bb_band_to_bidiag_host(a.n, a.b, bb.api.bb_dtype(a.dtype), 1, pin.data_ptr(), a.b + 1,
                                       a.n * (a.b + 1), dh.data_ptr(), dh.stride(0), eh.data_ptr(), eh.stride(0),
-                                      cfg.c(), stream.cuda_stream)
+                                      head.cfg.c(), head.stream.cuda_stream)
         e2e_step()
-        k = max(1, min(a.steps, 3))
         times = []
-        for _ in range(k):
+        for _ in range(max(1, min(a.steps, 3))):
             flush.fill_(1.0)
             torch.cuda.synchronize()
-            if world > 1:
-                dist.barrier()
+            barrier()
             t0 = time.perf_counter()
             e2e_step()
             times.append(time.perf_counter() - t0)
-        tt = float(np.mean(times))
-        if world > 1:
-            tq = torch.tensor([tt], dtype=torch.float64, device=dev)
-            dist.all_reduce(tq, op=dist.ReduceOp.MAX)
-            tt = float(tq.item())
+        tt = max_over_ranks(float(np.mean(times)))
         e2e = {"value": alg_bytes_step / tt / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": int(pin.numel() * pin.element_size()),
-               "d2h_bytes_per_step": int(B * (2 * a.n - 1) * pin.element_size()),
+               "d2h_bytes_per_step": int((2 * a.n - 1) * pin.element_size()),
                "ms_per_step": tt * 1e3, "api": "bb_band_to_bidiag_host (C ABI, pinned host buffers)",
                "timing": "host wall clock around the blocking call, max over ranks"}
+    launches = head.launches * a.steps
+    del head
 
+    # ---------------------------------------------------------------- batched: config 5 split across ranks
+    batched = None
+    if not a.no_batched:
+        start, count = partition(a.batch, world, rank)
+        counts = [partition(a.batch, world, r)[1] for r in range(world)]
+        rb = Runner(bb, torch, dev, a.batched_n, a.batched_b, "f64", 32, list(range(start, start + count)),
+                    seed=a.seed)
+        bsteps = 1
+        s_ms, p_ms = rb.timed(bsteps, 1, flush, barrier)
+        ms_b = max_over_ranks(float(np.mean(s_ms)))
+        # the one data-path collective: all-gather of (d, e), timed on its own
+        g_ms = None
+        if world > 1:
+            torch.cuda.synchronize()
+            barrier()
+            g0 = torch.cuda.Event(enable_timing=True)
+            g1 = torch.cuda.Event(enable_timing=True)
+            g0.record()
+            gather_results(rb.d, rb.e[:, : a.batched_n - 1], world, counts=counts)
+            g1.record()
+            torch.cuda.synchronize()
+            g_ms = max_over_ranks(g0.elapsed_time(g1))
+        batched = record(rb, s_ms, p_ms, a.batch, ms=ms_b,
+                         label=f"batched {a.batch} x n={a.batched_n} b={a.batched_b} f64 tw=32 split over "
+                               f"{world} GPU(s) (BASELINE config 5, strong scaling)")
+        batched["per_gpu_gbs"] = batched["value"] / world
+        batched["gather_ms"] = g_ms
+        batched["steps"] = bsteps
+        batched["warmup"] = 1
+        names = [(k, f"c5_n{a.batched_n}_b{a.batched_b}_f64_s{a.seed}_m{m}")
+                 for k, m in enumerate(range(start, start + count)) if m in (0, a.batch - 1)]
+        batched["parity"] = rb.parity(names)
+        batched["launches"] = rb.launches * bsteps
+        if rank == 0 and world == 1 and not a.no_cpu_baseline:
+            mat_bytes = rb.st["alg_bytes"]
+            batched["cpu_baseline"] = batched_cpu(a.batched_n, a.batched_b, 32, mat_bytes,
+                                                  max(2.0, a.cpu_seconds / 3))
+        del rb
+
+    # ---------------------------------------------------------------- extra single-GPU records (N = 1)
+    extra = []
+    if world == 1 and not a.no_extra:
+        for (n, b, dt, tw, steps, tag) in [(32768, 128, "f32", 32, 2, "c4"), (1024, 32, "f64", 32, 5, "c2"),
+                                            (1024, 32, "f32", 32, 5, "c2"), (8192, 64, "f64", 32, 3, "c3"),
+                                            (8192, 64, "f32", 32, 3, "c3"), (8192, 64, "f16", 32, 3, "c3")]:
+            r = Runner(bb, torch, dev, n, b, dt, tw, [0], seed=a.seed)
+            s_ms, p_ms = r.timed(steps, 1, flush)
+            rec = record(r, s_ms, p_ms, 1, label=f"BASELINE config {tag[1]}: n={n} b={b} {dt} tw={tw}")
+            rec["steps"] = steps
+            rec["parity"] = r.parity([(0, f"{tag}_n{n}_b{b}_{dt}_s{a.seed}_m0")])
+            extra.append(rec)
+            del r
+
+    # ---------------------------------------------------------------- CPU baseline (rank 0, N = 1)
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        r = oracle_sample(bands_np[0], a.b, a.tw, a.dtype, a.cpu_seconds)
+        import synth
+        flags = _oracle_native_once()
+        band = synth.random_band(a.n, a.b, a.dtype, seed=a.seed, matrix_id=0)
+        r = oracle_sample(band, a.b, a.tw, a.dtype, a.cpu_seconds)
         cpu = {"value": r["gbs"], "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": r["sample"],
-               "seconds": r["seconds"]}
+               "seconds": r["seconds"], "build": flags, "host": host_info()}
 
     if rank == 0:
-        out = {"metric": "band_to_bidiag_effective_GBps", "value": value, "unit": "GB/s", "n_gpus": world,
+        roof = None
+        # roofline of the headline pass kernels (this rank's events)
+        peak, src = hbm_peak()
+        pm = np.mean(np.array(pass_ms), axis=0)
+        tot = float(np.sum(pm))
+        st = bb.plan(a.n, a.b, a.dtype, 1, bb.Config(tw=a.tw, max_blocks_per_sm=a.maxb))
+        ach = st["alg_bytes"] / (tot * 1e-3) / 1e9
+        key = f"{a.n}:{a.b}:{a.dtype}:{a.tw}:1"
+        tr = ncu_traffic(key)
+        roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": tr, "traffic_source": ("profiles/ncu_traffic.json[%s]" % key) if tr is not None else None,
+                "peak_source": src,
+                "kernel": "pass kernels of one step (pass_v5_kernel x3: unit kernel; pass_v6_kernel: segment ring, "
+                          "target bandwidth 1); achieved = algorithmic bytes of the passes / their summed CUDA-event "
+                          "time on the launching stream",
+                "alg_bytes_per_step_per_rank": st["alg_bytes"], "pass_ms_mean": [float(x) for x in pm],
+                "pass_share_of_step": tot / float(np.mean(step_ms))}
+        out = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
                "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-               "scaling": "weak" if a.workload == "single" else "strong", "vs_baseline": None,
-               "dtype": a.dtype,
-               "data": "synthetic: i.i.d. N(0,1) band entries (numpy Philox, seed %d), rounded to %s" % (a.seed, a.dtype),
-               "config": workload_config(a),
-               "gflops": gflops, "matrices_per_s": mps,
-               "alg_bytes_per_step": alg_bytes_step, "alg_flops_per_step": alg_flops_step,
-               "critical_cycles": st["critical_cycles"], "passes": P, "steps_per_matrix": st["steps"],
+               "scaling": "weak", "vs_baseline": None, "dtype": a.dtype,
+               "data": "synthetic: i.i.d. N(0,1) band entries (numpy Philox, seed %d, matrix id = rank), rounded "
+                       "to %s" % (a.seed, a.dtype),
+               "config": workload_config(a, world),
+               "gflops": st["alg_flops"] * world / (ms_per_step * 1e-3) / 1e9,
+               "matrices_per_s": world / (ms_per_step * 1e-3),
+               "alg_bytes_per_step": alg_bytes_step, "alg_flops_per_step": st["alg_flops"] * world,
+               "critical_cycles": st["critical_cycles"], "passes": st["passes"], "steps_per_matrix": st["steps"],
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
-               "gpu_launches": int(launches_per_step * a.steps),
+               "gpu_launches": int(launches), "parity": parity, "batched": batched, "extra": extra,
                "step_ms": step_ms}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def dry_run(a, world, rank):
+    """CPU harness check: process group (gloo), the batched partition and its
+    single all-gather of fixed-shape (d, e) buffers, and the JSON line --
+    no device work, no numbers."""
+    import torch
+    import torch.distributed as dist
+    from paper_2510_12705_b200.dist import gather_results, partition
+    if world > 1:
+        dist.init_process_group("gloo")
+    start, count = partition(a.batch, world, rank)
+    counts = [partition(a.batch, world, r)[1] for r in range(world)]
+    n = 8
+    d = torch.arange(start, start + count, dtype=torch.float64).repeat_interleave(n).reshape(count, n)
+    e = -d[:, : n - 1]
+    D, E = gather_results(d, e, world, counts=counts)
+    ok = bool(torch.equal(D[:, 0], torch.arange(a.batch, dtype=torch.float64)))
+    if rank == 0:
+        out = {"metric": METRIC, "value": None, "unit": "GB/s", "n_gpus": world, "steps": 0, "warmup": 0,
+               "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+               "dtype": a.dtype, "data": "dry run (no device work)", "config": workload_config(a, world),
+               "dry_run": True, "gather_ok": ok, "gathered_shape": list(D.shape)}
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()

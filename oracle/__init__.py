@@ -44,11 +44,31 @@ def build(force: bool = False) -> str:
     return _LIB
 
 
-def lib():
+def use_native_build(outdir: str) -> str | None:
+    """bench.py cpu_baseline only: compile the same C source with
+    ``-march=native`` into ``outdir`` and load that build instead.
+    The arithmetic is unchanged (-ffp-contract=off, no fast-math: gcc may not
+    reassociate or contract), only instruction selection.  Returns the flags
+    used, or None (the portable build stays loaded)."""
+    global _lib
+    path = os.path.join(outdir, "libbb_oracle_native.so")
+    flags = ["-O2", "-march=native", "-fPIC", "-shared", "-std=c11", "-ffp-contract=off", "-fno-fast-math"]
+    try:
+        os.makedirs(outdir, exist_ok=True)
+        subprocess.check_call(["gcc"] + flags + ["-o", path, _SRC, "-lm"], stderr=subprocess.DEVNULL)
+    except Exception:
+        return None
+    _lib = None
+    lib(path)
+    return " ".join(flags)
+
+
+def lib(path: str | None = None):
     global _lib
     if _lib is None:
-        build()
-        L = ctypes.CDLL(_LIB)
+        if path is None:
+            build()
+        L = ctypes.CDLL(path or _LIB)
         L.oracle_house.argtypes = [_i64, _dp, _dp, _dp, _dp]
         L.oracle_house.restype = None
         L.oracle_num_passes.argtypes = [_i64, _i64, _i64]
