@@ -198,10 +198,10 @@ def host_info():
 
 
 # --------------------------------------------------------------------------- CPU oracle
-def _oracle_native_once():
+def _oracle_native_once(compile=True):
     import oracle
     if not getattr(_oracle_native_once, "done", False):
-        _oracle_native_once.flags = oracle.use_native_build("/tmp/bb_oracle_native") or \
+        _oracle_native_once.flags = oracle.use_native_build("/tmp/bb_oracle_native", compile=compile) or \
             "-O2 -ffp-contract=off (portable build)"
         _oracle_native_once.done = True
     return _oracle_native_once.flags
@@ -232,7 +232,7 @@ def oracle_sample(band, b, tw, dtype, budget_s):
 def _batched_cpu_worker(args):
     n, b, tw, mid, budget = args
     import synth
-    _oracle_native_once()
+    _oracle_native_once(compile=False)  # built once by the parent
     band = synth.random_band(n, b, "f64", seed=0, matrix_id=mid)
     return oracle_sample(band, b, tw, "f64", budget)
 
@@ -241,6 +241,7 @@ def batched_cpu(n, b, tw, mat_bytes, budget):
     """P = min(64, cores) oracle processes at once, one matrix each, a bounded
     sample per process; host matrices/s = P / (per-matrix bytes / per-process rate)."""
     from multiprocessing import get_context
+    _oracle_native_once()
     P = max(1, min(64, os.cpu_count() or 1))
     t0 = time.perf_counter()
     with get_context("spawn").Pool(P) as pool:

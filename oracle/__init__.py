@@ -44,7 +44,7 @@ def build(force: bool = False) -> str:
     return _LIB
 
 
-def use_native_build(outdir: str) -> str | None:
+def use_native_build(outdir: str, compile: bool = True) -> str | None:
     """bench.py cpu_baseline only: compile the same C source with
     ``-march=native`` into ``outdir`` and load that build instead.
     The arithmetic is unchanged (-ffp-contract=off, no fast-math: gcc may not
@@ -54,8 +54,12 @@ def use_native_build(outdir: str) -> str | None:
     path = os.path.join(outdir, "libbb_oracle_native.so")
     flags = ["-O2", "-march=native", "-fPIC", "-shared", "-std=c11", "-ffp-contract=off", "-fno-fast-math"]
     try:
-        os.makedirs(outdir, exist_ok=True)
-        subprocess.check_call(["gcc"] + flags + ["-o", path, _SRC, "-lm"], stderr=subprocess.DEVNULL)
+        if compile:
+            os.makedirs(outdir, exist_ok=True)
+            subprocess.check_call(["gcc"] + flags + ["-o", path + ".tmp", _SRC, "-lm"], stderr=subprocess.DEVNULL)
+            os.replace(path + ".tmp", path)
+        elif not os.path.exists(path):
+            return None
     except Exception:
         return None
     _lib = None
