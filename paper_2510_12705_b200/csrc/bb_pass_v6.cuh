@@ -51,11 +51,36 @@
 
 namespace bb {
 
+#ifndef BB_V6_POLL
+#define BB_V6_POLL 20 // ns between polls of a chunk barrier (0: suspended try_wait)
+#endif
 constexpr int V6_GMAX = 16;
 // chunk-loaded events: the producer runs up to R chunks ahead of WG 0, so the
 // ring of "chunk m loaded" mbarriers must be longer than R (a phase seen
 // twice would hang the waiter); the host caps R below this
 constexpr int V6_FRING = 64;
+// wait for a chunk-loaded phase: polled with test_wait + a short sleep (a
+// suspended try_wait is not reliably woken by TMA complete_tx; measured
+// multi-microsecond late wake-ups)
+__device__ __forceinline__ bool mb_test_wait(uint64_t *b, unsigned par)
+{
+    unsigned ok;
+    asm volatile("{\n\t.reg .pred P1;\n\t"
+                 "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, P1;\n\t}"
+                 : "=r"(ok)
+                 : "r"(su32(b)), "r"(par)
+                 : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void chunk_wait(uint64_t *b, unsigned par)
+{
+    if (BB_V6_POLL) {
+        while (!mb_test_wait(b, par)) __nanosleep(BB_V6_POLL);
+    } else {
+        mb_wait(b, par);
+    }
+}
 __device__ __forceinline__ uint64_t *fring_slot(uint64_t *ring, int K, unsigned &par)
 {
     par = (unsigned)(K / V6_FRING) & 1u;
@@ -153,14 +178,14 @@ __device__ __forceinline__ void step_v6(const PassArgsV6 &a, typename ComputeOf<
         if (g == 0) {
             unsigned par;
             uint64_t *b = fring_slot(y.barF, y.fbase + j, par); // chunk j loaded
-            mb_wait(b, par);
+            chunk_wait(b, par);
         } else {
             wait_prog(y, g - 1, min(2 * j + 4, 2 * Jprev));
         }
     }
     nbar_sync(bar, NT);
-    if (tr && tid == 0) tr[4] = gtimer();
-#define PROBE6(i_) do { if (tr && tid == 0) tr[i_] = clock64(); } while (0)
+    if (tr && tid == 0) tr[g == 0 ? 4 : 7] = gtimer();
+#define PROBE6(i_) do { if (tr && tid == 0 && g == 0) tr[i_] = clock64(); } while (0)
     PROBE6(8);
 
     // ---------------------------------------------------------------- right application (A)
@@ -204,14 +229,14 @@ __device__ __forceinline__ void step_v6(const PassArgsV6 &a, typename ComputeOf<
             if (p + c <= n - 1) { // chunk j+1 exists: loaded?
                 unsigned par;
                 uint64_t *b = fring_slot(y.barF, y.fbase + j + 1, par);
-                mb_wait(b, par);
+                chunk_wait(b, par);
             }
         } else {
             wait_prog(y, g - 1, min(2 * j + 5, 2 * Jprev));
         }
     }
     nbar_sync(bar, NT);
-    if (tr && tid == 0) tr[5] = gtimer();
+    if (tr && tid == 0 && g == 0) tr[5] = gtimer();
     PROBE6(12);
 
     // ---------------------------------------------------------------- left application (B)
@@ -379,7 +404,7 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v6_kernel(PassArgsV6 a, const _
                     const int xb = (p - r0 - 1) % NB;
                     const bool full = p + MT - 1 <= n - 1;
                     if (g == 0 && tid == 0) TRACE6(0, j);
-                    unsigned long long *tr = (a.trace && g == 0 && mat == 0 && k < a.trace_groups && j < a.trace_steps)
+                    unsigned long long *tr = (a.trace && g <= 1 && mat == 0 && k < a.trace_groups && j < a.trace_steps)
                                                  ? a.trace + ((int64_t)k * a.trace_steps + j) * 16
                                                  : nullptr;
                     if (full && xb + MT <= NB)

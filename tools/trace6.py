@@ -48,6 +48,9 @@ def summarize(path):
     for nm, (a0, a1) in zip(names, pairs):
         print("  cycles %-42s %7.0f" % (nm, np.median(cy[:, a1] - cy[:, a0])))
     print("  cycles A-post..B-start (incl. B wait) %7.0f" % np.median(cy[:, 12] - cy[:, 11]))
+    d1 = tr[k, 2:ns - 6, 7] - tr[k, 3:ns - 5, 6]
+    print("  WG1 A(j) start (after wait) - WG0 step j+1 end: median %.2f us" % (np.median(d1) / 1e3))
+    print("  WG1 A(j) start - WG0 A(j) start: median %.2f us" % (np.median(tr[k, 2:ns - 6, 7] - tr[k, 2:ns - 6, 4]) / 1e3))
     print("  WG0 step period median %.2f us, last-WG step period %.2f us" % (np.median(s0) / 1e3, np.median(s1) / 1e3))
     print("  last WG done(j) - WG0 start(j): median %.2f us" % (np.median(tr[k, 2:ns - 4, 1] - tr[k, 2:ns - 4, 0]) / 1e3))
     print("  pub(j) - lastdone(j): median %.2f us" % (np.median(tr[k, 2:ns - 4, 3] - tr[k, 2:ns - 4, 1]) / 1e3))
@@ -59,3 +62,14 @@ def summarize(path):
 if __name__ == "__main__":
     for p in sys.argv[1:]:
         summarize(p)
+
+
+def dump(path, k=None, j0=None, nj=8):
+    (ng, ns, c, t, G, grid), tr = read(path)
+    k = k if k is not None else ng // 2
+    j0 = j0 if j0 is not None else ns // 2
+    t0 = tr[k, j0, 0]
+    print("   j   WG0:start  Await-done  Bwait-done  stepend | WG1 Await-done | lastdone  pub")
+    for j in range(j0, j0 + nj):
+        r = (tr[k, j] - t0) / 1e3
+        print("%5d %9.2f %9.2f %9.2f %9.2f | %9.2f | %9.2f %9.2f" % (j, r[0], r[4], r[5], r[6], r[7], r[1], r[3]))
