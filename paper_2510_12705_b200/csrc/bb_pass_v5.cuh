@@ -326,36 +326,54 @@ __device__ __forceinline__ bool v5_scalars(C alpha, C q, C &tau, C &rho, C &beta
 // 44, a dependent fp64 compare 30 -- so "x[1:] == 0" is decided from the sum
 // of squares (an explicit test only when that sum is 0) and the safe-range
 // test is integer (v5_scalars).  ~880 cycles per link (tools/ubench/panel5.cu).
+// own[k*ks] = a[k] - wr * x[k*ks], k = 1 .. MT-1 (own and x are different
+// members of the panel: __restrict__ lets every load issue ahead of the
+// stores instead of one load-use-store round trip per element)
+template <class C, int MT>
+__device__ __forceinline__ void v5_axpy(C *__restrict__ own, const C *__restrict__ x, int ks, C wr, const C (&a)[MT])
+{
+    C xv[MT];
+#pragma unroll
+    for (int k = 1; k < MT; ++k) xv[k] = x[k * ks];
+#pragma unroll
+    for (int k = 1; k < MT; ++k) own[k * ks] = fma(-wr, xv[k], a[k]);
+}
+
 template <class C, int MT, int GT>
 __device__ __forceinline__ void v5_panel(C *pan, int ks, int ls, C *vs, int VP, C * /*xb*/, int lane)
 {
+    // Only the member's own vector a[] lives in registers; the source x is
+    // read from shared memory (broadcast) for the sums and again for the
+    // update -- keeping x in registers as well (2 x MT doubles) spilled the
+    // fp64 kernel to local memory inside this chain (ncu: ~95 LDL/STL per link).
     const bool member = lane < GT;
 #pragma unroll 1
     for (int g = 0; g < GT; ++g) {
         C *src = pan + g * ks + g * ls; // element (g) of member g
         C *own = pan + g * ks + lane * ls;    // element (g) of member lane
         const bool upd = member && lane > g;
-        C x[MT], a[MT];
+        // fp32: x is also kept in registers (no register pressure: faster);
+        // fp64: re-read for the update (x + a in registers spilled)
+        constexpr bool XREG = sizeof(C) == 4;
+        C a[MT], xr[XREG ? MT : 1];
 #pragma unroll
-        for (int k = 0; k < MT; ++k) x[k] = src[k * ks];
-        if (upd) {
-#pragma unroll
-            for (int k = 0; k < MT; ++k) a[k] = own[k * ks];
-        }
-        const C xl = (lane < MT) ? src[lane * ks] : C(0);
+        for (int k = 0; k < MT; ++k) a[k] = upd ? own[k * ks] : C(0);
         C q4[4] = {0, 0, 0, 0}, s4[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int k = 1; k < MT; ++k) {
-            q4[k & 3] = fma(x[k], x[k], q4[k & 3]);
-            s4[k & 3] = fma(a[k], x[k], s4[k & 3]);
+            const C xk = src[k * ks];
+            if constexpr (XREG) xr[k] = xk;
+            q4[k & 3] = fma(xk, xk, q4[k & 3]);
+            s4[k & 3] = fma(a[k], xk, s4[k & 3]);
         }
+        const C alpha = src[0];
+        const C xl = (lane < MT) ? src[lane * ks] : C(0);
+        const C x32 = (MT > 32) ? src[(MT > 32 ? 32 : 0) * ks] : C(0);
         const C ss = (q4[0] + q4[1]) + (q4[2] + q4[3]);
-        const C alpha = x[0];
         C tau = 0, rho = 0, beta = alpha;
         bool nz = ss > C(0);
         if (!nz) { // rare: all squares underflowed or x[1:] == 0
-#pragma unroll
-            for (int k = 1; k < MT; ++k) nz |= (x[k] != C(0));
+            for (int k = 1; k < MT; ++k) nz |= (src[k * ks] != C(0));
         }
         C *v = vs + g * VP;
         bool slow = nz && !v5_scalars<C>(alpha, ss, tau, rho, beta);
@@ -366,24 +384,30 @@ __device__ __forceinline__ void v5_panel(C *pan, int ks, int ls, C *vs, int VP, 
             beta = __shfl_sync(0xffffffffu, beta, 0);
             tau = v[MT];
             rho = C(1);
-#pragma unroll
-            for (int k = 1; k < MT; ++k) x[k] = v[k];
             s4[0] = s4[1] = s4[2] = s4[3] = C(0);
-#pragma unroll
-            for (int k = 1; k < MT; ++k) s4[k & 3] = fma(a[k], x[k], s4[k & 3]);
+            for (int k = 1; k < MT; ++k) s4[k & 3] = fma(a[k], v[k], s4[k & 3]);
         }
         if (upd && nz) {
             const C w = tau * fma(rho, (s4[0] + s4[1]) + (s4[2] + s4[3]), a[0]);
             const C wr = w * rho;
             own[0] = a[0] - w;
+            if (!slow) {
+                if constexpr (XREG) {
 #pragma unroll
-            for (int k = 1; k < MT; ++k) own[k * ks] = fma(-wr, x[k], a[k]);
+                    for (int k = 1; k < MT; ++k) own[k * ks] = fma(-wr, xr[k], a[k]);
+                } else {
+                    v5_axpy<C, MT>(own, src, ks, wr, a);
+                }
+            } else {
+                v5_axpy<C, MT>(own, v, 1, wr, a);
+            }
         }
         if (!slow) {
             if (lane < MT) v[lane] = (lane == 0) ? C(1) : (nz ? rho * xl : C(0));
-            if (MT > 32 && lane == 0) v[32] = nz ? rho * x[MT > 32 ? 32 : 0] : C(0);
+            if (MT > 32 && lane == 0) v[32] = nz ? rho * x32 : C(0);
             if (lane == 0) v[MT] = tau;
         }
+        __syncwarp(); // every lane has finished reading the source (update)
         if (lane < MT) src[lane * ks] = (lane == 0) ? beta : C(0);
         if (MT > 32 && lane == 0) src[32 * ks] = C(0);
         __syncwarp();
