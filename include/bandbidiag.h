@@ -68,7 +68,7 @@
 extern "C" {
 #endif
 
-#define BB_VERSION 200 /* 0.2.0: multi-sweep pass kernel (v4), half-step wavefront rules */
+#define BB_VERSION 300 /* 0.3.0: unit (v5) and segment-ring (v6) pass kernels, stage-3 singular values */
 
 /* Diagnostics read from the environment at call time (never needed for normal
  * use; results are bitwise independent of BB_V4_G):
@@ -205,6 +205,28 @@ bb_status bb_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const bb_
  * gpu_launches count. */
 bb_status bb_launch_count(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const bb_config *cfg,
                           int64_t *launches);
+
+/* ---- SVD stage 3 on the device ----------------------
+ * Singular values of the upper bidiagonal B = bidiag(d, e) that stage 2
+ * returns (the paper hands (d, e) to LAPACK BDSDC): bisection
+ * on the Golub-Kahan tridiagonal (zero diagonal, off-diagonal d_0, e_0, d_1,
+ * ..., d_{n-1}, eigenvalues +-sigma_i) with Sturm counts, one thread per
+ * singular value, fp64 arithmetic for every dtype; each sigma_i to within
+ * ~2 ulp of itself or eps * ||T||_Gershgorin (the normwise bound).
+ *   d: n elements, e: n-1 elements (DEVICE, dtype), sigma: n fp64 (DEVICE),
+ *   written in DESCENDING order.  Batched: matrix k at d + k*stride_d,
+ *   e + k*stride_e, sigma + k*stride_sigma (elements).
+ *   workspace: DEVICE, >= bb_bidiag_svals_workspace_size() bytes, caller-owned.
+ * Errors: BB_ERR_INVALID_VALUE (negative sizes, NULL pointers with n > 0,
+ * short workspace, overlapping batch strides), BB_ERR_NOT_SUPPORTED (dtype,
+ * n > 2^28, batch > 65535), BB_ERR_CUDA (launch failure).  Enqueued on
+ * `stream`, no host synchronisation. */
+bb_status bb_bidiag_svals_workspace_size(int64_t n, int64_t batch, size_t *bytes);
+bb_status bb_bidiag_svals(int64_t n, bb_dtype dtype, const void *d, const void *e, double *sigma, void *workspace,
+                          size_t workspace_bytes, void *stream);
+bb_status bb_bidiag_svals_batched(int64_t n, bb_dtype dtype, int64_t batch, const void *d, int64_t stride_d,
+                                  const void *e, int64_t stride_e, double *sigma, int64_t stride_sigma,
+                                  void *workspace, size_t workspace_bytes, void *stream);
 
 const char *bb_status_string(bb_status s);
 int32_t bb_version(void);

@@ -29,7 +29,8 @@ BB_FLAG_NO_SEGMENT_KERNEL = 0x8
 EXPORTED = [
     "bb_band_to_bidiag", "bb_band_to_bidiag_batched", "bb_band_to_bidiag_ex",
     "bb_band_to_bidiag_batched_ex", "bb_band_to_bidiag_host", "bb_workspace_size", "bb_plan",
-    "bb_launch_count", "bb_status_string", "bb_version",
+    "bb_launch_count", "bb_status_string", "bb_version", "bb_bidiag_svals", "bb_bidiag_svals_batched",
+    "bb_bidiag_svals_workspace_size",
 ]
 
 
@@ -78,6 +79,10 @@ def lib() -> ctypes.CDLL:
         L.bb_workspace_size.argtypes = [_i64, _i64, i, _i64, _cfgp, ctypes.POINTER(ctypes.c_size_t)]
         L.bb_plan.argtypes = [_i64, _i64, i, _i64, _cfgp, ctypes.POINTER(bb_plan_stats)]
         L.bb_launch_count.argtypes = [_i64, _i64, i, _i64, _cfgp, ctypes.POINTER(_i64)]
+        L.bb_bidiag_svals.argtypes = [_i64, i, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]
+        L.bb_bidiag_svals_batched.argtypes = [_i64, i, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, ctypes.c_size_t,
+                                              _vp]
+        L.bb_bidiag_svals_workspace_size.argtypes = [_i64, _i64, ctypes.POINTER(ctypes.c_size_t)]
         L.bb_status_string.argtypes = [i]
         L.bb_status_string.restype = ctypes.c_char_p
         L.bb_version.argtypes = []
@@ -151,3 +156,15 @@ def bb_launch_count(n, b, dtype, batch=1, cfg=None) -> int:
 
 def bb_version() -> int:
     return lib().bb_version()
+
+
+def bb_bidiag_svals_workspace_size(n, batch=1) -> int:
+    out = ctypes.c_size_t()
+    _check(lib().bb_bidiag_svals_workspace_size(n, batch, ctypes.byref(out)), "bb_bidiag_svals_workspace_size")
+    return out.value
+
+
+def bb_bidiag_svals_batched(n, dtype, batch, d, stride_d, e, stride_e, sigma, stride_sigma, workspace,
+                            workspace_bytes, stream):
+    _check(lib().bb_bidiag_svals_batched(n, dtype, batch, d, stride_d, e, stride_e, sigma, stride_sigma,
+                                         workspace, workspace_bytes, stream), "bb_bidiag_svals_batched")

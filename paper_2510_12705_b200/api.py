@@ -184,3 +184,26 @@ def band_to_bidiag_host(band, b: int, tw: int | None = None, cfg: Config | None 
                              e.data_ptr(), e.stride(0), _cfg(cfg, tw).c(), _stream())
     e = e[:, : max(n - 1, 0)]
     return (d[0], e[0]) if single else (d, e)
+
+
+def bidiag_svals(d: torch.Tensor, e: torch.Tensor) -> torch.Tensor:
+    """SVD stage 3 on the device: singular values of the upper
+    bidiagonal(s) (d, e) -- d: (n,) or (batch, n), e: (n-1,) or (batch, n-1),
+    CUDA tensors of one dtype -- as fp64, descending, shape like d.
+    Bisection on the Golub-Kahan tridiagonal in bb_svals.cu."""
+    if not d.is_cuda or not e.is_cuda:
+        raise ValueError("d, e must be CUDA tensors")
+    single = d.dim() == 1
+    D = d.unsqueeze(0) if single else d
+    E = e.unsqueeze(0) if single else e
+    B, n = D.shape
+    D = D.contiguous()
+    E = E.contiguous() if E.numel() else torch.zeros(B, 1, dtype=D.dtype, device=D.device)
+    _check_same(D, E)
+    sig = torch.empty(B, n, dtype=torch.float64, device=D.device)
+    nb = N.bb_bidiag_svals_workspace_size(n, B)
+    ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=D.device)
+    with torch.cuda.device(D.device):
+        N.bb_bidiag_svals_batched(n, bb_dtype(D), B, D.data_ptr(), D.stride(0), E.data_ptr(), E.stride(0),
+                                  sig.data_ptr(), n, ws.data_ptr(), nb, _stream(D.device))
+    return sig[0] if single else sig

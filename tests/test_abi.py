@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_version_and_status_strings():
-    assert bb.bb_version() == 200
+    assert bb.bb_version() == 300
     for s in range(6):
         assert N.status_string(s).startswith("BB_")
 
@@ -132,3 +132,18 @@ def test_launch_count():
     assert N.bb_launch_count(1024, 1, N.BB_F64) == 2
     cyc = N.bb_launch_count(64, 8, N.BB_F64, 1, N.bb_config(4, 0, 0, 0, N.BB_SCHED_CYCLE, 0))
     assert cyc == 2 + oracle.workload(64, 8, 4, 8)["critical_cycles"]
+
+
+def test_svals_validation_is_synchronous():
+    # SVD stage 3 entry points: argument errors are reported before any device work
+    nb = N.bb_bidiag_svals_workspace_size(100, 2)
+    assert nb == 8 * (2 * 2 * 100 + 2 * 2)
+    L = N.lib()
+    fake = 0x1000
+    assert L.bb_bidiag_svals(-1, N.BB_F64, fake, fake, fake, fake, 1 << 20, None) == N.BB_ERR_INVALID_VALUE
+    assert L.bb_bidiag_svals(10, 7, fake, fake, fake, fake, 1 << 20, None) == N.BB_ERR_NOT_SUPPORTED
+    assert L.bb_bidiag_svals(10, N.BB_F64, fake, fake, fake, fake, 8, None) == N.BB_ERR_INVALID_VALUE
+    assert L.bb_bidiag_svals(10, N.BB_F64, None, fake, fake, fake, 1 << 20, None) == N.BB_ERR_INVALID_VALUE
+    assert L.bb_bidiag_svals(0, N.BB_F64, None, None, None, None, 0, None) == N.BB_SUCCESS
+    assert L.bb_bidiag_svals_batched(10, N.BB_F64, 2, fake, 5, fake, 9, fake, 10, fake, 1 << 20,
+                                     None) == N.BB_ERR_INVALID_VALUE   # overlapping d strides
