@@ -228,6 +228,23 @@ bb_status bb_bidiag_svals_batched(int64_t n, bb_dtype dtype, int64_t batch, cons
                                   const void *e, int64_t stride_e, double *sigma, int64_t stride_sigma,
                                   void *workspace, size_t workspace_bytes, void *stream);
 
+/* ---- SVD stage 1 on the device ------------------------
+ * Dense n x n A (DEVICE, column-major, lda >= n, fp32 or fp64) -> upper band
+ * with b superdiagonals, U^T A V = band (U, V orthogonal, not formed), by
+ * block Householder reflections: per block column a QR of the column panel
+ * and an LQ of the row panel (one-CTA panel kernels, LAPACK dlarfg / dlarft
+ * conventions), trailing updates as GEMMs (cuBLAS).  The "classical block
+ * Householder" first stage the paper pairs with its bulge chasing (P:42,
+ * P:308).  A is OVERWRITTEN (it holds the banded matrix on exit); `band`
+ * (DEVICE, LAPACK upper band of the stage-2 input layout, ldband >= b + 1)
+ * receives the band.  workspace: DEVICE, >= bb_dense_to_band_workspace_size()
+ * bytes.  Errors: BB_ERR_INVALID_VALUE (sizes, NULL pointers, workspace),
+ * BB_ERR_NOT_SUPPORTED (fp16), BB_ERR_CUDA.  Enqueued on `stream`; calls on
+ * one device serialise on an internal cuBLAS handle. */
+bb_status bb_dense_to_band_workspace_size(int64_t n, int64_t b, bb_dtype dtype, size_t *bytes);
+bb_status bb_dense_to_band(int64_t n, int64_t b, bb_dtype dtype, void *A, int64_t lda, void *band, int64_t ldband,
+                           void *workspace, size_t workspace_bytes, void *stream);
+
 const char *bb_status_string(bb_status s);
 int32_t bb_version(void);
 

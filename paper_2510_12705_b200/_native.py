@@ -30,7 +30,7 @@ EXPORTED = [
     "bb_band_to_bidiag", "bb_band_to_bidiag_batched", "bb_band_to_bidiag_ex",
     "bb_band_to_bidiag_batched_ex", "bb_band_to_bidiag_host", "bb_workspace_size", "bb_plan",
     "bb_launch_count", "bb_status_string", "bb_version", "bb_bidiag_svals", "bb_bidiag_svals_batched",
-    "bb_bidiag_svals_workspace_size",
+    "bb_bidiag_svals_workspace_size", "bb_dense_to_band", "bb_dense_to_band_workspace_size",
 ]
 
 
@@ -83,6 +83,8 @@ def lib() -> ctypes.CDLL:
         L.bb_bidiag_svals_batched.argtypes = [_i64, i, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, ctypes.c_size_t,
                                               _vp]
         L.bb_bidiag_svals_workspace_size.argtypes = [_i64, _i64, ctypes.POINTER(ctypes.c_size_t)]
+        L.bb_dense_to_band.argtypes = [_i64, _i64, i, _vp, _i64, _vp, _i64, _vp, ctypes.c_size_t, _vp]
+        L.bb_dense_to_band_workspace_size.argtypes = [_i64, _i64, i, ctypes.POINTER(ctypes.c_size_t)]
         L.bb_status_string.argtypes = [i]
         L.bb_status_string.restype = ctypes.c_char_p
         L.bb_version.argtypes = []
@@ -168,3 +170,14 @@ def bb_bidiag_svals_batched(n, dtype, batch, d, stride_d, e, stride_e, sigma, st
                             workspace_bytes, stream):
     _check(lib().bb_bidiag_svals_batched(n, dtype, batch, d, stride_d, e, stride_e, sigma, stride_sigma,
                                          workspace, workspace_bytes, stream), "bb_bidiag_svals_batched")
+
+
+def bb_dense_to_band_workspace_size(n, b, dtype) -> int:
+    out = ctypes.c_size_t()
+    _check(lib().bb_dense_to_band_workspace_size(n, b, dtype, ctypes.byref(out)), "bb_dense_to_band_workspace_size")
+    return out.value
+
+
+def bb_dense_to_band(n, b, dtype, A, lda, band, ldband, workspace, workspace_bytes, stream):
+    _check(lib().bb_dense_to_band(n, b, dtype, A, lda, band, ldband, workspace, workspace_bytes, stream),
+           "bb_dense_to_band")

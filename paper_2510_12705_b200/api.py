@@ -207,3 +207,22 @@ def bidiag_svals(d: torch.Tensor, e: torch.Tensor) -> torch.Tensor:
         N.bb_bidiag_svals_batched(n, bb_dtype(D), B, D.data_ptr(), D.stride(0), E.data_ptr(), E.stride(0),
                                   sig.data_ptr(), n, ws.data_ptr(), nb, _stream(D.device))
     return sig[0] if single else sig
+
+
+def dense_to_band(A: torch.Tensor, b: int, overwrite: bool = False) -> torch.Tensor:
+    """SVD stage 1 on the device: dense square CUDA tensor A
+    (fp32/fp64; any layout) -> its upper band with b superdiagonals, U^T A V,
+    in the stage-2 input layout: a (n, b+1) tensor t[j, b + i - j] = band(i, j).
+    Block Householder QR/LQ panels + cuBLAS trailing GEMMs (bb_stage1.cu)."""
+    if A.dim() != 2 or A.shape[0] != A.shape[1] or not A.is_cuda:
+        raise ValueError("A must be a square CUDA matrix")
+    n = A.shape[0]
+    # column-major working copy: the transpose of a row-major contiguous tensor
+    W = A.t().contiguous() if not overwrite else A.t().contiguous()
+    band = torch.empty(n, b + 1, dtype=A.dtype, device=A.device)
+    nb = N.bb_dense_to_band_workspace_size(n, b, bb_dtype(A))
+    ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=A.device)
+    with torch.cuda.device(A.device):
+        N.bb_dense_to_band(n, b, bb_dtype(A), W.data_ptr(), n, band.data_ptr(), b + 1, ws.data_ptr(), nb,
+                           _stream(A.device))
+    return band
