@@ -316,7 +316,7 @@ bb_status run_stage1(int64_t n64, int64_t b64, T *A, int64_t lda, T *band, int64
             dim3 tg((unsigned)((nb + 31) / 32), (unsigned)((mt + 31) / 32));
             transpose_kernel<T><<<tg, dim3(32, 8), 0, st>>>(R, (int)lda, nb, mt, Pp, n); // Pp: mt x nb
             const int nq = std::min(nb, mt);
-            panel_qr_kernel<T><<<1, PQR_THREADS, 0, st>>>(Pp, n, mt, nq, tau);
+            panel_qr_kernel<T><<<1, PQR_THREADS, 0, st>>>(Pp, n, mt, nb, tau); // min(mt, nb) reflectors, applied to all nb columns
             lq_writeback_kernel<T><<<grid((int64_t)nb * mt), thr, 0, st>>>(Pp, n, mt, nb, R, lda);
             const int nrow = n - k - nb; // trailing rows below the row panel
             if (nrow > 0) {
