@@ -520,6 +520,36 @@ def main():
             extra.append(rec)
             del r
 
+    # ---------------------------------------------------------------- stage 3 and small-n batched (N = 1)
+    stage3 = None
+    small_batched = None
+    if world == 1 and not a.no_extra:
+        # SVD stage 3 on the device (F3): singular values of the headline bidiagonal
+        r = Runner(bb, torch, dev, a.n, a.b, a.dtype, a.tw, [0], seed=a.seed)
+        r.step()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        bb.bidiag_svals(r.d[0], r.e[0, : a.n - 1])
+        times = []
+        for _ in range(3):
+            ev0.record()
+            sig = bb.bidiag_svals(r.d[0], r.e[0, : a.n - 1])
+            ev1.record()
+            torch.cuda.synchronize()
+            times.append(ev0.elapsed_time(ev1))
+        stage3 = {"workload": f"singular values of the n={a.n} bidiagonal (bisection, fp64)", "ms": float(np.median(times))}
+        from tests.golden_util import golden_path, load
+        gname = f"c4_n{a.n}_b{a.b}_{a.dtype}_s{a.seed}_m0"
+        if os.path.exists(golden_path(gname)):
+            g = load(gname)
+            stage3["max_abs_err_over_normF_vs_oracle"] = float(np.max(np.abs(sig.cpu().numpy() - g["sigma"]))) / g["fro"]
+        del r
+        # F2: many small matrices at the paper's crossover size, interleaved in the same launches
+        nsm = 512
+        r = Runner(bb, torch, dev, 1024, 32, "f64", 32, list(range(nsm)), seed=a.seed)
+        s_ms, p_ms = r.timed(2, 1, flush)
+        small_batched = record(r, s_ms, p_ms, nsm, label=f"batched {nsm} x n=1024 b=32 f64 tw=32 (config 2 size)")
+        del r
+
     # ---------------------------------------------------------------- CPU baseline (rank 0, N = 1)
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -560,6 +590,7 @@ def main():
                "critical_cycles": st["critical_cycles"], "passes": st["passes"], "steps_per_matrix": st["steps"],
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
                "gpu_launches": int(launches), "parity": parity, "batched": batched, "extra": extra,
+               "stage3": stage3, "small_batched": small_batched,
                "step_ms": step_ms}
         print(json.dumps(out), flush=True)
     if world > 1:
