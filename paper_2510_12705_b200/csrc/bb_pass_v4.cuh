@@ -122,6 +122,11 @@ __device__ __forceinline__ void mb_init(uint64_t *b, unsigned count)
 {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count) : "memory");
 }
+// make mbarrier initialisations visible before first use (by other threads)
+__device__ __forceinline__ void fence_mbarrier_init()
+{
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
 __device__ __forceinline__ void mb_inval(uint64_t *b)
 {
     asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(su32(b)) : "memory");
@@ -619,8 +624,10 @@ __device__ __forceinline__ void step_v4(const PassArgsV4 &a, S *Wg, int mat, int
             const int rlo = max(s.q0, jc - c - t), rhi = min(min(s.p0 + WT - 1, jc + t), n - 1);
             S *gcol = Wg + (ku - jc) + (int64_t)jc * ldw;
             for (int i = rlo + lane; i <= rhi; i += 32) {
-                C v = *tcell(i, jc);
-                if (i == s.q && jc >= s.p && jc <= s.hi) v = (jc == s.p) ? beta1 : C(0);
+                // this WG's own x row is being rewritten by tid 0: take it from beta1
+                // without reading the cell (no read-write race on shared memory)
+                const bool xrow = i == s.q && jc >= s.p && jc <= s.hi;
+                const C v = xrow ? ((jc == s.p) ? beta1 : C(0)) : *tcell(i, jc);
                 stg(gcol + i, v);
             }
         }
@@ -696,8 +703,9 @@ __device__ __forceinline__ void step_v4(const PassArgsV4 &a, S *Wg, int mat, int
         for (int e = tid; e < tot; e += NT) {
             const int i = s.p0 + ii, jc = s.p0 + k, off = jc - i;
             if (i < n && jc < n && off >= -t && off <= c + t) {
-                C v = k < WT ? curT[(i - s.trow0) * TP + k] : curW[(k - WT) * TP + ii];
-                if (jc == s.p && i >= s.p && i <= s.hi) v = (i == s.p) ? beta2 : C(0);
+                const bool ycol = jc == s.p && i >= s.p && i <= s.hi; // own y column: from beta2
+                const C v = ycol ? ((i == s.p) ? beta2 : C(0))
+                                 : (k < WT ? curT[(i - s.trow0) * TP + k] : curW[(k - WT) * TP + ii]);
                 stg(Wg + (ku + i) + (int64_t)jc * (ldw - 1), v);
             }
             ii += dii;
@@ -749,6 +757,7 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v4_kernel(PassArgsV4 a)
     const int total = a.batch * a.ngroups;
     for (int i = threadIdx.x; i < NBAR; i += blockDim.x)
         mb_init(bars + i, i >= 2 * V4_GMAX * V4_RING ? (unsigned)npt : 1u);
+    fence_mbarrier_init();
     if (threadIdx.x < V4_GMAX) ebase_s[threadIdx.x] = 0;
     if (threadIdx.x == 0) fbase_s = 0;
     int prev_r0 = -1;

@@ -358,6 +358,7 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v6_kernel(PassArgsV6 a, const _
     const int total = a.batch * a.ngroups;
     for (int i = threadIdx.x; i < NBAR; i += blockDim.x)
         mb_init(bars + i, (i >= 2 * V6_GMAX * V4_RING && !TMA) ? 32u : 1u);
+    fence_mbarrier_init();
     if (threadIdx.x < V6_GMAX) ebase_s[threadIdx.x] = 0;
     if (threadIdx.x == 0) fbase_s = 0;
     int prev_r0 = -1, prev_M = 0;
