@@ -50,13 +50,16 @@ struct PassArgsV2 {
     int trace_sweeps, trace_steps;
 };
 
+// named barriers, non-.aligned forms: a warp may reach them diverged (e.g.
+// after a tid == 0 branch) -- bar.sync (= barrier.sync.aligned) requires a
+// converged warp (compute-sanitizer synccheck: "Divergent thread(s)")
 __device__ __forceinline__ void nbar_sync(int id, int count)
 {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+    asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 __device__ __forceinline__ void nbar_arrive(int id, int count)
 {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+    asm volatile("barrier.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
 enum { BAR_START = 1, BAR_C = 2, BAR_A = 3, BAR_W1 = 4, BAR_B = 5 };
