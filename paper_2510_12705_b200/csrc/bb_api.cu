@@ -226,7 +226,8 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
                 if (const char *e = getenv("BB_V6_G")) gcap = std::max(0, std::min(16, atoi(e)));
                 const size_t chunk = cs * (size_t)cc * (size_t)(3 * cc); // TMA box: 3c rows x c columns
                 const size_t budget = (size_t)kSmemOptinFallback - 10240; // static: barriers, counters, x staging
-                for (int G = std::min(gcap, 14); G >= 1; --G) { // named barriers 1 + g <= 15
+                for (int G = std::min(std::min(gcap, 14), cc); G >= 1; --G) { // named barriers 1 + g <= 15; G <= c
+                    // (the writer's finality rule, tests/test_v6_protocol.py)
                     if (G * nt + 64 > ntmax) continue;
                     // WG g trails WG g-1 by ~2 steps in steady state; the ring holds
                     // the chunks from the last WG's position to WG 0's B window,
