@@ -58,13 +58,23 @@ __device__ __forceinline__ int ld_relaxed(const int *p)
     return v;
 }
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-// spin until *p >= need: relaxed polling, one acquire fence on success
-__device__ __forceinline__ void wait_geq(const int *p, int need)
+// poll interval for a progress flag: short when the awaited value is close,
+// long when the producer is far behind -- a CTA whose predecessor has not
+// started yet must not hammer the flag's L2 line (hundreds of such pollers
+// slowed the active groups' L2 traffic, measured)
+__device__ __forceinline__ unsigned poll_ns(int have, int need, int near)
 {
-    if (ld_relaxed(p) < need) {
-        while (ld_relaxed(p) < need) {
-            __nanosleep(32);
-        }
+    return (need - have > near) ? 1024u : 32u;
+}
+// spin until *p >= need: relaxed polling, one acquire fence on success
+__device__ __forceinline__ void wait_geq(const int *p, int need, int near = 2)
+{
+    int v = ld_relaxed(p);
+    if (v < need) {
+        do {
+            __nanosleep(poll_ns(v, need, near));
+            v = ld_relaxed(p);
+        } while (v < need);
     }
     fence_acq_rel();
 }

@@ -510,13 +510,15 @@ __device__ __forceinline__ void st_vec(C *b, int m, const C (&v)[MT])
 __device__ __forceinline__ void wait_geq_v4(const int *p, int need, int dbg_tag, const int *prog_s = nullptr,
                                             int r0 = 0, int glast = 0)
 {
-    if (ld_relaxed(p) < need) {
+    int v = ld_relaxed(p);
+    if (v < need) {
         const unsigned long long t0 = BB_V4_WATCHDOG ? gtimer() : 0ull;
-        while (ld_relaxed(p) < need) {
-            __nanosleep(32);
+        while (v < need) {
+            __nanosleep(poll_ns(v, need, 4)); // far behind (> 2 steps): sleep ~1 us
+            v = ld_relaxed(p);
             if (BB_V4_WATCHDOG && gtimer() - t0 > 2000000000ull) {
                 printf("v4 watchdog: global wait need %d have %d tag %d block %d r0 %d glast %d prog %d %d %d\n", need,
-                       ld_relaxed(p), dbg_tag, (int)blockIdx.x, r0, glast, prog_s ? prog_s[0] : -1,
+                       v, dbg_tag, (int)blockIdx.x, r0, glast, prog_s ? prog_s[0] : -1,
                        prog_s ? prog_s[1] : -1, prog_s ? prog_s[2] : -1);
                 while (ld_relaxed(p) < need) __nanosleep(1000);
                 break;

@@ -73,3 +73,21 @@ def dump(path, k=None, j0=None, nj=8):
     for j in range(j0, j0 + nj):
         r = (tr[k, j] - t0) / 1e3
         print("%5d %9.2f %9.2f %9.2f %9.2f | %9.2f | %9.2f %9.2f" % (j, r[0], r[4], r[5], r[6], r[7], r[1], r[3]))
+
+
+def periods(path):
+    (ng, ns, c, t, G, grid), tr = read(path)
+    out = []
+    for k in [0, 1, 2, 3, 5, 10, 20, 50, 100, 200, 500, 1000, 2000, 3000, 4000]:
+        if k >= ng:
+            break
+        valid = np.nonzero(tr[k, :, 0] > 0)[0]
+        if len(valid) < 16:
+            continue
+        J = valid[-1] + 1
+        s0 = tr[k, 2:J - 4, 0]
+        per = np.median(np.diff(s0)) / 1e3
+        bw = np.median(tr[k, 2:J - 4, 5] - tr[k, 2:J - 4, 4]) / 1e3
+        out.append((k, per, bw))
+        print("group %5d: WG0 step period %.2f us, A+Bwait %.2f us" % (k, per, bw))
+    return out
