@@ -233,7 +233,9 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
                     // the chunks from the last WG's position to WG 0's B window,
                     // as many as shared memory allows (slack absorbs jitter)
                     const int rmin = 3 + 2 * (G - 1);
-                    const int R = (int)std::min<size_t>(std::min<size_t>(budget / chunk, (size_t)rmin + 8), 48); // < V6_FRING
+                    int R = (int)std::min<size_t>(std::min<size_t>(budget / chunk, (size_t)rmin + 4), 48); // < V6_FRING;
+                    // slack 4: larger rings measured slower for fp32 (smaller L1 carve-out)
+                    if (const char *e = getenv("BB_V6_R")) R = std::max(rmin, std::min(R, atoi(e))); // experiments
                     if (R < rmin) continue;
                     pp.g6 = G;
                     pp.r6 = R;
@@ -251,7 +253,23 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
     P.cfg = cfg;
     size_t es = elem_size(dtype);
     P.band_bytes = align_up((size_t)batch * (size_t)P.mat_stride * es);
-    P.flag_bytes = align_up((size_t)P.passes.size() * (size_t)batch * (size_t)n * sizeof(int));
+    {
+        // flags: per pass batch x (groups or sweeps) x stride ints; group flags one
+        // per 128-byte line unless that would exceed 1/8 of the band storage
+        int stride = 32;
+        for (;; stride /= 2) {
+            int64_t off = 0;
+            for (PassPlan &pp : P.passes) {
+                const bool grp = pp.g5 > 0 || pp.g6 > 0;
+                const int64_t nf = grp ? (pp.g5 > 0 ? pp.ngroups5 : pp.ngroups6) : n;
+                pp.fstride = grp ? stride : 1;
+                pp.flag_off = off;
+                off += (int64_t)batch * std::max<int64_t>(nf, 1) * pp.fstride;
+            }
+            P.flag_bytes = align_up((size_t)off * sizeof(int));
+            if (stride == 1 || P.flag_bytes * 8 <= (size_t)batch * (size_t)P.mat_stride * elem_size(dtype)) break;
+        }
+    }
     P.counter_bytes = align_up(std::max<size_t>(1, P.passes.size()) * sizeof(int));
     P.total = P.band_bytes + P.flag_bytes + P.counter_bytes;
     return BB_SUCCESS;

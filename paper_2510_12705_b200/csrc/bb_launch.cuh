@@ -101,7 +101,7 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
         a.s = pp.s;
         a.batch = batch;
         a.nsweeps = pp.nsweeps;
-        a.progress = flags + (int64_t)pi * batch * n;
+        a.progress = flags + pp.flag_off;
         a.counter = counters + pi;
         a.LT = pp.LT;
         a.LW = pp.LW;
@@ -132,6 +132,7 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
             a5.batch = batch;
             a5.nsweeps = pp.nsweeps;
             a5.ngroups = pp.ngroups5;
+            a5.fstride = pp.fstride;
             a5.progress = a.progress;
             a5.counter = a.counter;
             a5.LA = pp.LA5;
@@ -192,6 +193,7 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
             a6.batch = batch;
             a6.nsweeps = pp.nsweeps;
             a6.ngroups = pp.ngroups6;
+            a6.fstride = pp.fstride;
             a6.progress = a.progress;
             a6.counter = a.counter;
             constexpr bool F64 = sizeof(typename bb::ComputeOf<S>::type) == 8;

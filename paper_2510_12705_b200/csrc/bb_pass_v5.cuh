@@ -63,7 +63,8 @@ struct PassArgsV5 {
     int c, t, G;
     int a0, b0;
     int batch, nsweeps, ngroups;
-    int *progress; // [batch][ngroups], half-units
+    int *progress; // [batch][ngroups] x fstride, half-units
+    int fstride;   // ints between consecutive group flags
     int *counter;
     int LA, LB; // shared pitches (odd, in elements of C)
     unsigned long long *trace;
@@ -453,8 +454,8 @@ __global__ void __launch_bounds__(256, 1) pass_v5_kernel(PassArgsV5 a)
         const int r0 = k * G;
         const int J = sweep_len(n, c, t, r0);
         S *Wg = reinterpret_cast<S *>(a.W) + (int64_t)mat * a.mat_stride;
-        const int *pprev = k > 0 ? a.progress + (int64_t)mat * a.ngroups + (k - 1) : nullptr;
-        int *pme = a.progress + (int64_t)mat * a.ngroups + k;
+        const int *pprev = k > 0 ? a.progress + ((int64_t)mat * a.ngroups + (k - 1)) * a.fstride : nullptr;
+        int *pme = a.progress + ((int64_t)mat * a.ngroups + k) * a.fstride;
         const int Jp = k > 0 ? sweep_len(n, c, t, r0 - G) : 0;
 
         for (int j = 0; j < J; ++j) {

@@ -93,7 +93,8 @@ struct PassArgsV6 {
     int ldw, ku, n;
     int c, t, G, R;
     int batch, nsweeps, ngroups;
-    int *progress; // [batch][ngroups] half-steps of each group's last sweep
+    int *progress; // [batch][ngroups] x fstride: half-steps of each group's last sweep
+    int fstride;   // ints between consecutive group flags
     int *counter;
     unsigned long long *trace;
     int trace_groups, trace_steps;
@@ -390,7 +391,8 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v6_kernel(PassArgsV6 a, const _
         S *Wg = reinterpret_cast<S *>(a.W) + (int64_t)mat * a.mat_stride;
         const int64_t ldw = a.ldw;
         const int ku = a.ku;
-        int *gprog = a.progress + (int64_t)mat * a.ngroups;
+        int *gprog = a.progress + (int64_t)mat * a.ngroups * a.fstride;
+        const int fs = a.fstride;
 
         if ((int)threadIdx.x < ncomp) {
             // ------------------------------------------------ compute WGs
@@ -420,7 +422,7 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v6_kernel(PassArgsV6 a, const _
             // ------------------------------------------------ PRODUCER warp: chunk loads
             const int lane = threadIdx.x & 31;
             const int Jp = r0 > 0 ? sweep_len(n, c, t, r0 - 1) : 0;
-            const int *pprev = k > 0 ? gprog + (k - 1) : nullptr;
+            const int *pprev = k > 0 ? gprog + (int64_t)(k - 1) * fs : nullptr;
             for (int mm = 0; mm < M; ++mm) {
                 if (lane == 0) {
                     // ring slot of chunk mm - R free (written back)
@@ -475,7 +477,7 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v6_kernel(PassArgsV6 a, const _
                 if (lane == 0) {
                     fence_proxy_async(); // async-proxy global writes -> generic release
                     fence_acq_rel();
-                    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(gprog + k), "r"(v) : "memory");
+                    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(gprog + (int64_t)k * fs), "r"(v) : "memory");
                     wb_s = wb;
                 }
             };

@@ -50,6 +50,12 @@ struct PassPlan {
     // segment-ring kernel (bb_pass_v6.cuh): target bandwidth 1, G sweeps per CTA
     int g6 = 0, r6 = 0, nt6 = 0, ngroups6 = 0;
     size_t smem6 = 0;
+    // progress flags of this pass: offset (ints) into the flag region, stride
+    // (ints) between consecutive flags -- one L2 line per group flag for the
+    // unit / segment-ring kernels (neighbouring groups' flags sharing a line
+    // are written and polled concurrently), 1 for the per-sweep kernels
+    int64_t flag_off = 0;
+    int fstride = 1;
 };
 
 struct Plan {
