@@ -12,6 +12,9 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libbandbidiag.so")
+# A/B experiments only: load another build of the same library
+if os.environ.get("BB_LIB_PATH"):
+    LIB_PATH = os.environ["BB_LIB_PATH"]
 
 BB_F16, BB_F32, BB_F64 = 0, 1, 2
 BB_SUCCESS = 0

@@ -263,7 +263,7 @@ __device__ void bulge_step(const PassArgs &a, int mat, int r, int j, typename Co
     C *scal = v + (t + 1);           // tau, beta (x2)
 
     S *W = reinterpret_cast<S *>(a.W) + (int64_t)mat * a.mat_stride;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ku = a.ku;
     const int64_t ldw = a.ldw;
 

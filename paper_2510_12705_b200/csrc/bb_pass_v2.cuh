@@ -349,9 +349,6 @@ __global__ void __launch_bounds__(NTMAX) pass_v2_kernel(PassArgsV2 a)
     const bool is_poll = (warp == (ntc >> 5));
     const bool is_rel = (warp == (ntc >> 5) + 1);
     const int n = a.n, c = a.c, t = a.t;
-    const int64_t ldw = a.ldw;
-    const int ku = a.ku;
-    const int LW = a.LW;
     const int total = a.batch * a.nsweeps;
 
     for (;;) {
