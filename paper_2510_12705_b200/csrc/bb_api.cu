@@ -205,11 +205,23 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
                 }
                 if (pp.g5 > 0) {
                     // inter-group rule of the unit kernel: exact hazard search over its
-                    // load / write-back rectangles (tools/v5_rules.py): A half waits for
-                    // progress[k-1] >= 2j + a5, B half for >= 2j + b5
-                    const bool tight = 2 * pp.g5 <= c - t;
-                    pp.a5 = tight ? 2 : 4;
-                    pp.b5 = tight ? 4 : 5;
+                    // load / write-back rectangles (tools/v5_rules.py,
+                    // tests/test_unit_schedule.py): A half waits for progress[k-1] >=
+                    // 2j + a5, B half for >= 2j + b5 -- (2, 3) when 3G <= c - t, with
+                    // 2j + 4 while the predecessor's unit j+1 is its last one (that unit
+                    // writes back its whole H region); (2, 4) when 2G <= c - t; else (4, 5)
+                    const int G5 = pp.g5;
+                    if (3 * G5 <= c - t) {
+                        pp.a5 = 2;
+                        pp.b5 = 3;
+                        pp.b5t = 4;
+                    } else if (2 * G5 <= c - t) {
+                        pp.a5 = 2;
+                        pp.b5 = pp.b5t = 4;
+                    } else {
+                        pp.a5 = 4;
+                        pp.b5 = pp.b5t = 5;
+                    }
                     pp.nt5 = (int)std::min<int64_t>(256, std::max<int64_t>(64, (c + t + 31) / 32 * 32));
                     pp.ngroups5 = (int)((ns + pp.g5 - 1) / pp.g5);
                 }

@@ -129,6 +129,7 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
             a5.G = pp.g5;
             a5.a0 = pp.a5;
             a5.b0 = pp.b5;
+            a5.b0t = pp.b5t;
             a5.batch = batch;
             a5.nsweeps = pp.nsweeps;
             a5.ngroups = pp.ngroups5;

@@ -65,7 +65,7 @@ struct PassArgsV5 {
     int64_t mat_stride;
     int ldw, ku, n;
     int c, t, G;
-    int a0, b0;
+    int a0, b0, b0t; // B wait 2j + b0, or 2j + b0t while the predecessor's unit j+1 is its last
     int batch, nsweeps, ngroups;
     int *progress; // [batch][ngroups] x fstride, half-units
     int fstride;   // ints between consecutive group flags
@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(256, 1) pass_v5_kernel(PassArgsV5 a)
             }
             TRACE5(5);
             // ------------------------------------------------ B half
-            if (tid == 0 && pprev) wait_geq(pprev, min(2 * j + a.b0, 2 * Jp));
+            if (tid == 0 && pprev) wait_geq(pprev, min(2 * j + (j + 2 < Jp ? a.b0 : a.b0t), 2 * Jp));
             __syncthreads();
             TRACE5(6);
             v5_load<S, C>(Wg, ku, ldw1, n, c, t, p, W, p + W, c, Hr, LB, tid, nthr);

@@ -45,7 +45,7 @@ struct PassPlan {
     int a4 = 0, b4 = 0; // v4 half-step wait offsets (refined for target bandwidth < 4, tools/depcheck.py)
     size_t smem4 = 0;
     // unit kernel (bb_pass_v5.cuh): G sweeps per CTA advanced one step at a time
-    int g5 = 0, nt5 = 0, LA5 = 0, LB5 = 0, a5 = 0, b5 = 0, ngroups5 = 0;
+    int g5 = 0, nt5 = 0, LA5 = 0, LB5 = 0, a5 = 0, b5 = 0, b5t = 0, ngroups5 = 0;
     size_t smem5 = 0;
     // segment-ring kernel (bb_pass_v6.cuh): target bandwidth 1, G sweeps per CTA
     int g6 = 0, r6 = 0, nt6 = 0, ngroups6 = 0;

@@ -67,10 +67,29 @@ def test_lockstep_units_break_target_bandwidth_one():
         assert np.max(np.abs(off)) > 1e-3   # fill-in left behind: not a valid reduction
 
 
-@pytest.mark.parametrize("c,t,G", [(32, 16, 8), (48, 16, 16), (24, 8, 8), (40, 16, 16), (64, 32, 16)])
+def _rule(c, t, G):
+    # bb_api.cu (unit kernel): (a0, b0, b0 while the predecessor is in its last unit)
+    if 3 * G <= c - t:
+        return 2, 3, 4
+    if 2 * G <= c - t:
+        return 2, 4, 4
+    return 4, 5, 5
+
+
+@pytest.mark.parametrize("c,t,G", [(32, 16, 8), (48, 16, 16), (24, 8, 8), (40, 16, 16), (64, 32, 16), (64, 32, 8),
+                                   (128, 32, 32), (96, 32, 16), (36, 12, 8), (50, 14, 12)])
 def test_inter_group_rule_is_safe(c, t, G):
-    tight = 2 * G <= c - t
-    a0, b0 = (2, 4) if tight else (4, 5)          # bb_api.cu (unit kernel)
+    a0, b0, b0t = _rule(c, t, G)
     n = 8 * c + 10 * G + 7
-    for nn in (n, n + c // 2 + 1):
-        assert R.safe(nn, c, t, G, a0, b0, kmax=3)
+    for nn in (n, n + c // 2 + 1, n + G + 2, n + c + 5):
+        assert R.safe(nn, c, t, G, a0, b0, kmax=3, tail_b0=b0t)
+
+
+@pytest.mark.parametrize("c,t,G", [(96, 32, 32), (64, 32, 16), (128, 32, 32)])
+def test_shorter_rules_are_unsafe(c, t, G):
+    # the hazard search is not vacuous: one half-step less than the rule used fails
+    a0, b0, b0t = _rule(c, t, G)
+    n = 8 * c + 10 * G + 7
+    res = [R.safe(nn, c, t, G, a0, b0 - 1, kmax=3, tail_b0=b0t) and R.safe(nn, c, t, G, a0, b0, kmax=3, tail_b0=b0t - 1)
+           for nn in (n, n + c // 2 + 1, n + c + 5)]
+    assert not all(res)

@@ -70,7 +70,17 @@ def need_of(h, a0, b0):
     return (h - 2) + b0
 
 
-def safe(n, c, t, G, a0, b0, dmax=None, kmax=4):
+def need_of_tail(h, a0, b0, Jp, tail_b0=4):
+    """need_of with the end-of-predecessor refinement: the B half of unit j
+    waits for 2j + b0 while the predecessor's unit j+1 is not its last unit,
+    for 2j + tail_b0 otherwise (its last unit writes back the whole H region)"""
+    if h % 2 == 1:
+        return (h - 1) + a0
+    j = h // 2 - 1
+    return 2 * j + (b0 if j + 2 < Jp else tail_b0)
+
+
+def safe(n, c, t, G, a0, b0, dmax=None, kmax=4, tail_b0=None):
     ns = max(0, (n - 2) - (c - t) + 1)
     ng = (ns + G - 1) // G
     if ng < 2:
@@ -82,14 +92,15 @@ def safe(n, c, t, G, a0, b0, dmax=None, kmax=4):
     for k in range(min(kmax, ng - 1)):
         for d in range(1, min(dmax, ng - 1 - k) + 1):
             kp = k + d
+            nf = (lambda hh, Jp: need_of(hh, a0, b0)) if tail_b0 is None else \
+                (lambda hh, Jp: need_of_tail(hh, a0, b0, Jp, tail_b0))
             for (h, L, Wr) in P[kp]:
                 # guaranteed progress of groups kp-1, ..., k
-                g = need_of(h, a0, b0)
-                ok_chain = True
+                g = nf(h, Jk[kp - 1])
                 for e in range(1, d):
                     g = min(g, 2 * Jk[kp - e])
                     # group kp-e has progress >= g: it executed the phase with value g
-                    g = need_of(g, a0, b0)
+                    g = nf(g, Jk[kp - e - 1])
                 g = min(g, 2 * Jk[k])
                 for (h2, L2, W2) in P[k]:
                     if h2 <= g:
