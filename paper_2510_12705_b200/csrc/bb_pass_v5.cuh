@@ -54,10 +54,6 @@
 
 #include <type_traits>
 
-#ifndef BB_V5_REG_PANEL
-#define BB_V5_REG_PANEL 1 // 1: fp32 panel rows in registers (v5_panel_reg); 2: also fp64 (experiment)
-#endif
-
 namespace bb {
 
 struct PassArgsV5 {
@@ -419,92 +415,6 @@ __device__ __forceinline__ void v5_panel(C *pan, int ks, int ls, C *vs, int VP, 
     }
 }
 
-// fp32 panel with the members' rows in REGISTERS (lane l = member l): the
-// source row of link g is broadcast by shuffles from lane g instead of a
-// shared-memory store / barrier / load round trip, and each lane's window
-// R[0..MT) slides by one element per link (register moves, static indices).
-// Same arithmetic in the same order as v5_panel (results bitwise equal).
-// Element e of member l starts at R[e]; after link g, R[0] (element g) is
-// final for every member and is stored; the tail is stored at the end.
-template <class C, int MT, int GT>
-__device__ __forceinline__ void v5_panel_reg(C *pan, int ks, int ls, C *vs, int VP, C *xb, int lane)
-{
-    constexpr int L = MT + GT - 1;
-    const bool member = lane < GT;
-    C R[L];
-#pragma unroll
-    for (int e = 0; e < L; ++e) R[e] = member ? pan[e * ks + lane * ls] : C(0);
-#pragma unroll 1
-    for (int g = 0; g < GT; ++g) {
-        const bool upd = member && lane > g;
-        C x[MT];
-#pragma unroll
-        for (int k = 0; k < MT; ++k) x[k] = __shfl_sync(0xffffffffu, R[k], g);
-        C q4[4] = {0, 0, 0, 0}, s4[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int k = 1; k < MT; ++k) {
-            q4[k & 3] = fma(x[k], x[k], q4[k & 3]);
-            s4[k & 3] = fma(upd ? R[k] : C(0), x[k], s4[k & 3]);
-        }
-        const C alpha = x[0];
-        const C ss = (q4[0] + q4[1]) + (q4[2] + q4[3]);
-        C tau = 0, rho = 0, beta = alpha;
-        bool nz = ss > C(0);
-        if (!nz) {
-#pragma unroll
-            for (int k = 1; k < MT; ++k) nz |= (x[k] != C(0));
-        }
-        C *v = vs + g * VP;
-        const bool slow = nz && !v5_scalars<C>(alpha, ss, tau, rho, beta);
-        if (slow) { // scaled reflector from the source row staged in shared memory
-            __syncwarp();
-            if (lane == g) {
-#pragma unroll
-                for (int k = 0; k < MT; ++k) xb[k] = R[k];
-            }
-            __syncwarp();
-            if (lane == 0) beta = v5_slow_link<C>(xb, 1, MT, v);
-            __syncwarp();
-            beta = __shfl_sync(0xffffffffu, beta, 0);
-            tau = v[MT];
-            rho = C(1);
-            s4[0] = s4[1] = s4[2] = s4[3] = C(0);
-            for (int k = 1; k < MT; ++k) s4[k & 3] = fma(upd ? R[k] : C(0), v[k], s4[k & 3]);
-        }
-        if (upd && nz) {
-            const C w = tau * fma(rho, (s4[0] + s4[1]) + (s4[2] + s4[3]), R[0]);
-            const C wr = w * rho;
-            R[0] = R[0] - w;
-            if (!slow) {
-#pragma unroll
-                for (int k = 1; k < MT; ++k) R[k] = fma(-wr, x[k], R[k]);
-            } else {
-#pragma unroll
-                for (int k = 1; k < MT; ++k) R[k] = fma(-wr, v[k], R[k]);
-            }
-        }
-        if (lane == g) {
-            if (!slow) {
-                v[0] = C(1);
-#pragma unroll
-                for (int k = 1; k < MT; ++k) v[k] = nz ? rho * x[k] : C(0);
-                v[MT] = tau;
-            }
-            R[0] = beta;
-#pragma unroll
-            for (int k = 1; k < MT; ++k) R[k] = C(0);
-        }
-        if (member) pan[g * ks + lane * ls] = R[0]; // element g: final for every member
-#pragma unroll
-        for (int e = 0; e + 1 < L; ++e) R[e] = R[e + 1];
-    }
-    if (member) {
-#pragma unroll
-        for (int e = 0; e + 1 < MT; ++e) pan[(GT + e) * ks + lane * ls] = R[e];
-    }
-    __syncwarp();
-}
-
 #define TRACE5(slot)                                                                                       \
     do {                                                                                                   \
         if (a.trace && tid == 0 && mat == 0 && k < a.trace_groups && j < a.trace_units)                   \
@@ -564,12 +474,7 @@ __global__ void __launch_bounds__(256, 1) pass_v5_kernel(PassArgsV5 a)
             }
             __syncthreads();
             TRACE5(2);
-            if (tid < 32) {
-                if constexpr ((std::is_same<C, float>::value || BB_V5_REG_PANEL > 1) && BB_V5_REG_PANEL)
-                    v5_panel_reg<C, MT, GT>(Win, LA, 1, vA, VP, xbuf, lane);
-                else
-                    v5_panel<C, MT, GT>(Win, LA, 1, vA, VP, xbuf, lane);
-            }
+            if (tid < 32) v5_panel<C, MT, GT>(Win, LA, 1, vA, VP, xbuf, lane);
             __syncthreads();
             TRACE5(3);
             // bulk rows q0+G .. p+W-1: reflector g applies iff i <= p + g + t
@@ -594,12 +499,7 @@ __global__ void __launch_bounds__(256, 1) pass_v5_kernel(PassArgsV5 a)
             v5_load_wait();
             __syncthreads();
             TRACE5(7);
-            if (tid < 32) {
-                if constexpr ((std::is_same<C, float>::value || BB_V5_REG_PANEL > 1) && BB_V5_REG_PANEL)
-                    v5_panel_reg<C, MT, GT>(Win + dq, 1, LA, vB, VP, xbuf, lane);
-                else
-                    v5_panel<C, MT, GT>(Win + dq, 1, LA, vB, VP, xbuf, lane);
-            }
+            if (tid < 32) v5_panel<C, MT, GT>(Win + dq, 1, LA, vB, VP, xbuf, lane);
             __syncthreads();
             TRACE5(8);
             // bulk columns p+G .. p+G+c+t-1: reflector g applies iff x <= p + g + t + c
