@@ -117,7 +117,9 @@ typedef enum {
  * Zero-initialise for defaults. */
 typedef struct {
     int32_t tw;                /* inner tilewidth TW; 0 = default (32, measured) */
-    int32_t threads_per_block; /* "Threads per block"; 0 = auto                 */
+    int32_t threads_per_block; /* "Threads per block" of the GENERIC step kernel */
+                               /* (BB_FLAG_GENERIC_KERNEL); 0 = auto.  The default      */
+                               /* kernels size their CTAs from (c, t, G) themselves     */
     int32_t max_blocks_per_sm; /* "Max blocks": resident CTAs per SM; 0 = auto  */
     int32_t dep_distance;      /* s; 0 = auto (2, or 3 when the pass target is 1);      */
                                /* values below auto are raised to auto                  */
@@ -143,7 +145,7 @@ typedef struct {
     double alg_bytes;        /* per matrix: 2 * elem_size * alg_elements (read + write)  */
     double alg_flops;        /* per matrix: sum 4m(hi-q) + 4m(ce-p) + 6m                 */
     int32_t tw;              /* resolved tilewidth                                       */
-    int32_t threads_per_block;
+    int32_t threads_per_block; /* threads per CTA the first pass's kernel launches          */
     int64_t ldw;             /* leading dimension of the working band (elements),        */
                              /* >= b_eff + 2 tw + 1, padded so ldw * elem is a multiple  */
                              /* of 16 bytes (TMA column boxes); mat_stride = n * ldw     */

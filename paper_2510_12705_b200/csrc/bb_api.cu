@@ -496,7 +496,14 @@ bb_status bb_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const bb_
     out->ku = P.ku;
     out->mat_stride = P.mat_stride;
     out->workspace_bytes = P.total;
-    out->threads_per_block = P.passes.empty() ? 0 : P.passes[0].threads;
+    if (!P.passes.empty()) { // threads per CTA the first pass launches
+        const PassPlan &p0 = P.passes[0];
+        out->threads_per_block = p0.g5 > 0   ? p0.nt5
+                                 : p0.g6 > 0 ? p0.nt6
+                                 : p0.g4 > 0 ? p0.g4 * p0.nt4 + 32 * (p0.pw4 + 1)
+                                 : p0.v2     ? p0.ntc + 64
+                                             : p0.threads;
+    }
     double elems = 0, flops = 0;
     int64_t steps = 0, crit = 0;
     for (const PassPlan &pp : P.passes) {

@@ -72,6 +72,12 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
 
     cudaEvent_t *ev = reinterpret_cast<cudaEvent_t *>(P.cfg.timing_events);
     auto mark = [&](int k) { if (ev) cudaEventRecord(ev[k], st); };
+    // every pass's shared-memory need is checked before any device work is
+    // enqueued (an unsupported configuration returns with nothing launched)
+    for (const PassPlan &pp : P.passes) {
+        const size_t need = pp.g5 > 0 ? pp.smem5 : pp.g6 > 0 ? pp.smem6 : pp.g4 > 0 ? pp.smem4 : pp.v2 ? pp.smem2 : pp.smem;
+        if (need > (size_t)di.smem_optin) return BB_ERR_NOT_SUPPORTED;
+    }
     if (!P.passes.empty()) {
         if (cudaMemsetAsync(flags, 0, P.flag_bytes + P.counter_bytes, st) != cudaSuccess) return BB_ERR_CUDA;
     }
