@@ -218,7 +218,8 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
             if (occ < 1) return BB_ERR_NOT_SUPPORTED;
             if (P.cfg.max_blocks_per_sm > 0) occ = std::min(occ, (int)P.cfg.max_blocks_per_sm);
             const int64_t tasks = (int64_t)pp.ngroups6 * batch;
-            const int64_t grid = std::min<int64_t>(tasks, (int64_t)occ * di.sms);
+            int64_t grid = std::min<int64_t>(tasks, (int64_t)occ * di.sms);
+            if (const char *e = getenv("BB_V6_GRID")) grid = std::max<int64_t>(1, std::min<int64_t>(grid, atoi(e))); // experiments
             const char *tf = getenv("BB_TRACE_FILE");
             const char *tp = getenv("BB_TRACE_PASS");
             unsigned long long *tbuf = nullptr;

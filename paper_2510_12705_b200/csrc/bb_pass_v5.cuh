@@ -415,6 +415,11 @@ __device__ __forceinline__ void v5_panel(C *pan, int ks, int ls, C *vs, int VP, 
     }
 }
 
+#define TRACE5T(slot)                                                                                      \
+    do {                                                                                                   \
+        if (a.trace && tid == 32 && mat == 0 && k < a.trace_groups && j < a.trace_units)                  \
+            a.trace[((int64_t)k * a.trace_units + j) * 16 + (slot)] = gtimer();                            \
+    } while (0)
 #define TRACE5(slot)                                                                                       \
     do {                                                                                                   \
         if (a.trace && tid == 0 && mat == 0 && k < a.trace_groups && j < a.trace_units)                   \
@@ -477,30 +482,49 @@ __global__ void __launch_bounds__(256, 1) pass_v5_kernel(PassArgsV5 a)
             if (tid < 32) v5_panel<C, MT, GT>(Win, LA, 1, vA, VP, xbuf, lane);
             __syncthreads();
             TRACE5(3);
-            // bulk rows q0+G .. p+W-1: reflector g applies iff i <= p + g + t
-            for (int b = tid; b < dq + t; b += nthr) {
-                const int ii = G + b, i = q0 + ii;
-                v5_apply<C, MT, U>(Win + ii, LA, G, i - p - t, vA, VP);
+            // A bulk, split so that the B panel overlaps the rest of the A half:
+            // warps 1.. apply the G row reflectors to the rows of the B panel
+            // (rows [p, p+W): the B panel needs nothing else -- its cells came with
+            // the V load, and no other group touches them before our write-back)
+            // first and release warp 0 at named barrier 1; warp 0 then runs the B
+            // panel while warps 1.. finish the other bulk rows, write back the A
+            // region, publish 2j+1, take the B wait and load H.
+            // Bulk rows: q0+G .. p+W-1 (reflector g applies iff i <= p + g + t).
+            if (tid >= 32) {
+                const int nw = nthr - 32, tt = tid - 32;
+                const int nrows = dq + t; // b in [0, dq + t): row q0 + G + b
+                bool arrived = false;
+                for (int bp = tt; bp < nrows; bp += nw) {
+                    if (!arrived && bp >= W) {
+                        nbar_arrive(1, nthr);
+                        arrived = true;
+                    }
+                    const int b = bp < W ? dq - G + bp : bp - W; // B-panel rows first
+                    const int ii = G + b, i = q0 + ii;
+                    v5_apply<C, MT, U>(Win + ii, LA, G, i - p - t, vA, VP);
+                }
+                if (!arrived) nbar_arrive(1, nthr);
+                nbar_sync(2, nw); // every A row done
+                TRACE5T(4);
+                v5_store<S, C>(Wg, ku, ldw1, n, c, t, q0, dq, p, W, Win, LA, tt, nw);
+                nbar_sync(2, nw);
+                if (tt == 0) {
+                    fence_acq_rel();
+                    st_release(pme, 2 * j + 1);
+                    TRACE5T(5);
+                    // ------------------------------------------------ B half
+                    if (pprev) wait_geq(pprev, min(2 * j + (j + 2 < Jp ? a.b0 : a.b0t), 2 * Jp));
+                    TRACE5T(6);
+                }
+                nbar_sync(2, nw);
+                v5_load<S, C>(Wg, ku, ldw1, n, c, t, p, W, p + W, c, Hr, LB, tt, nw);
+                v5_load_wait();
+                TRACE5T(7);
+            } else {
+                nbar_sync(1, nthr); // rows [p, p+W) of the A bulk done
+                v5_panel<C, MT, GT>(Win + dq, 1, LA, vB, VP, xbuf, lane);
             }
-            __syncthreads();
-            TRACE5(4);
-            v5_store<S, C>(Wg, ku, ldw1, n, c, t, q0, dq, p, W, Win, LA, tid, nthr);
-            __syncthreads();
-            if (tid == 0) {
-                fence_acq_rel();
-                st_release(pme, 2 * j + 1);
-            }
-            TRACE5(5);
-            // ------------------------------------------------ B half
-            if (tid == 0 && pprev) wait_geq(pprev, min(2 * j + (j + 2 < Jp ? a.b0 : a.b0t), 2 * Jp));
-            __syncthreads();
-            TRACE5(6);
-            v5_load<S, C>(Wg, ku, ldw1, n, c, t, p, W, p + W, c, Hr, LB, tid, nthr);
-            v5_load_wait();
-            __syncthreads();
-            TRACE5(7);
-            if (tid < 32) v5_panel<C, MT, GT>(Win + dq, 1, LA, vB, VP, xbuf, lane);
-            __syncthreads();
+            __syncthreads(); // B panel, H load and the whole A half complete
             TRACE5(8);
             // bulk columns p+G .. p+G+c+t-1: reflector g applies iff x <= p + g + t + c
             for (int b = tid; b < c + t; b += nthr) {
