@@ -57,7 +57,12 @@ def _run(tool, n, extra=(), mode="all"):
     p = subprocess.run([_sanitizer(), "--tool", tool, *extra, sys.executable,
                         os.path.join(ROOT, "tests", "san_run.py")], capture_output=True, text=True, timeout=1500,
                        env=env, cwd=ROOT)
-    return p.returncode, p.stdout + p.stderr
+    out = p.stdout + p.stderr
+    if "compute-sanitizer is closed" in out or ("san_run ok" not in out and "closed on this pool" in out):
+        # the GPU pool disables compute-sanitizer (runs under it left GPUs needing a
+        # reset); the device-side bounds checks of tests/test_gpu_bounds.py stand in
+        pytest.skip("compute-sanitizer disabled on this GPU pool")
+    return p.returncode, out
 
 
 @pytest.mark.parametrize("tool,mode", [("memcheck", "all"), ("synccheck", "sync")])
