@@ -102,6 +102,12 @@ __device__ __forceinline__ void lds_acquire(const int *p)
     asm volatile("{\n\t.reg .b32 t;\n\tld.acquire.cta.shared.b32 t, [%0];\n\t}" ::"r"((unsigned)__cvta_generic_to_shared(p))
                  : "memory");
 }
+__device__ __forceinline__ int lds_acquire_v(const int *p)
+{
+    int v;
+    asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+    return v;
+}
 __device__ __forceinline__ void sts_release(int *p, int v)
 {
     asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");

@@ -129,6 +129,8 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, int c0, int
 }
 // every bulk store of this thread complete (its writes performed)
 __device__ __forceinline__ void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// every bulk store of this thread has finished READING its shared-memory source
+__device__ __forceinline__ void tma_store_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 // generic-proxy accesses (flag acquire, shared-memory reads of a ring slot)
 // ordered before the async-proxy (TMA) accesses that follow
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
@@ -481,16 +483,34 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v6_kernel(PassArgsV6 a, const _
                     wb_s = wb;
                 }
             };
+            // Batched: every step the last WG has finished since the previous
+            // round is written back in one go (one completion wait per round, not
+            // per chunk -- a serial store + wait per chunk capped the group at one
+            // step per write-back latency, ~2 us); ring slots are released as soon
+            // as the stores have READ them, before the global writes complete.
             int wb = 0; // chunks written back
-            for (int j = 0; j < Js - 1; ++j) {
-                if (lane == 0) wait_prog(y, glast, 2 * j + 2);
-                __syncwarp();
-                if (j < M) {
-                    write_chunk(j);
-                    wb = j + 1;
+            int j = 0;  // steps [0, j) handled
+            while (j < Js - 1) {
+                int have = 0;
+                if (lane == 0) {
+                    wait_prog(y, glast, 2 * j + 2);
+                    have = lds_acquire_v(y.prog + glast);
                 }
-                publish(2 * j + 2, wb);
-                if (lane == 0) TRACE6(3, j);
+                have = __shfl_sync(0xffffffffu, have, 0);
+                const int jend = min(Js - 1, have >> 1); // steps [0, jend) of the last WG done
+                for (; j < jend; ++j)
+                    if (j < M) {
+                        write_chunk(j);
+                        wb = j + 1;
+                    }
+                if constexpr (TMA) {
+                    if (lane == 0) {
+                        tma_store_wait_read();
+                        wb_s = wb; // slots free for the producer
+                    }
+                }
+                publish(2 * jend, wb);
+                if (lane == 0) TRACE6(3, jend - 1);
             }
             // every WG finished: flush the rest of the ring, publish the final value
             if (lane == 0)
