@@ -1,13 +1,13 @@
 # v6 (target-bandwidth-1 pass) timelines at several group sizes (tools/trace6.py)
 set -x
-for G in ${GS:-2 3 4}; do
+for G in ${GS:-3 4}; do
   BB_V6_G=$G timeout 200 python tools/trace_run6.py 32768 128 ${DT:-f64} 32 3 >> gpurun_out/tr6run.txt 2>&1
   mv gpurun_out/tr6_${DT:-f64}_n32768.bin gpurun_out/tr6_G$G.bin
-  python tools/trace6.py gpurun_out/tr6_G$G.bin > gpurun_out/tr6_summary_G$G.txt 2>&1
   python -c "
 import sys; sys.path.insert(0,'tools'); import trace6
-trace6.dump('gpurun_out/tr6_G$G.bin', k=2048, j0=500, nj=12)
+trace6.crossgroup('gpurun_out/tr6_G$G.bin', k=2048)
+trace6.crossgroup('gpurun_out/tr6_G$G.bin', k=1)
 trace6.periods('gpurun_out/tr6_G$G.bin')
-" >> gpurun_out/tr6_summary_G$G.txt 2>&1
+" > gpurun_out/tr6_cross_G$G.txt 2>&1
 done
 rm -f gpurun_out/tr6_*.bin

@@ -91,3 +91,26 @@ def periods(path):
         out.append((k, per, bw))
         print("group %5d: WG0 step period %.2f us, A+Bwait %.2f us" % (k, per, bw))
     return out
+
+
+def crossgroup(path, k=2048, j0=400, nj=200):
+    """Where WG0 of group k waits at B(j) (chunk j+1): the previous group's last
+    WG finishing step j+2, its writer publishing, our producer issuing, the TMA
+    landing -- medians over steps j0 .. j0+nj (absolute times, same clock)."""
+    (ng, ns, c, t, G, grid), tr = read(path)
+    rows = []
+    for j in range(j0, j0 + nj):
+        bstart = tr[k, j, 4]        # WG0 A wait done (A half starts)
+        bdone = tr[k, j, 5]         # WG0 B wait done
+        last = tr[k - 1, j + 2, 1]  # previous group's last WG finished step j+2
+        pub = tr[k - 1, j + 2, 3]   # its writer published step j+2 (0 if batched into a later round)
+        iss = tr[k, j + 1, 2]       # our producer issued chunk j+1
+        if min(bstart, bdone, last, iss) <= 0:
+            continue
+        rows.append((bdone - bstart, last - bstart, (pub - last) if pub > 0 else np.nan, iss - last, bdone - iss))
+    a = np.array(rows) / 1e3
+    names = ["B wait (A start -> B wait done)", "prev last done(j+2) - A start", "pub - prev last done",
+             "producer issue(j+1) - prev last done", "B wait done - issue (TMA + poll)"]
+    print(f"crossgroup k={k} G={G}: {len(rows)} steps")
+    for i, nm in enumerate(names):
+        print("  %-40s median %7.2f us  mean %7.2f" % (nm, np.nanmedian(a[:, i]), np.nanmean(a[:, i])))
