@@ -158,6 +158,11 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
                 return BB_ERR_CUDA;
             if (occ < 1) return BB_ERR_NOT_SUPPORTED;
             if (P.cfg.max_blocks_per_sm > 0) occ = std::min(occ, (int)P.cfg.max_blocks_per_sm);
+            // one matrix, fp32 compute: a second co-resident CTA slows both groups'
+            // panel chains more than it adds sweeps in flight (measured: n = 8192,
+            // b = 64: 35.0 -> 29.8 ms; n = 32768 pass 3: 210 -> 206 ms); fp64 keeps
+            // the occupancy (n = 32768 pass 3: 164 vs 181 ms at one CTA per SM)
+            else if (batch == 1 && sizeof(typename bb::ComputeOf<S>::type) == 4) occ = 1;
             const int64_t tasks = (int64_t)pp.ngroups5 * batch;
             const int64_t grid = std::min<int64_t>(tasks, (int64_t)occ * di.sms);
             const char *tf = getenv("BB_TRACE_FILE");
@@ -225,6 +230,7 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
             unsigned long long *tbuf = nullptr;
             if (tf && (int)pi == (tp ? atoi(tp) : 0)) {
                 a6.trace_groups = std::min(pp.ngroups6, 4096);
+                a6.trace_ring = getenv("BB_TRACE_RING") ? 1 : 0;
                 a6.trace_steps = (int)sweep_len_h(n, pp.c, pp.t, 0) + 1;
                 size_t tb = (size_t)a6.trace_groups * a6.trace_steps * 16 * sizeof(unsigned long long);
                 if (cudaMalloc(&tbuf, tb) == cudaSuccess) {

@@ -420,6 +420,11 @@ __device__ __forceinline__ void v5_panel(C *pan, int ks, int ls, C *vs, int VP, 
         if (a.trace && tid == 32 && mat == 0 && k < a.trace_groups && j < a.trace_units)                  \
             a.trace[((int64_t)k * a.trace_units + j) * 16 + (slot)] = gtimer();                            \
     } while (0)
+#define TRACE5C(slot)                                                                                      \
+    do {                                                                                                   \
+        if (a.trace && tid == 32 && mat == 0 && k < a.trace_groups && j < a.trace_units)                  \
+            a.trace[((int64_t)k * a.trace_units + j) * 16 + (slot)] = clock64();                           \
+    } while (0)
 #define TRACE5(slot)                                                                                       \
     do {                                                                                                   \
         if (a.trace && tid == 0 && mat == 0 && k < a.trace_groups && j < a.trace_units)                   \
@@ -506,11 +511,16 @@ __global__ void __launch_bounds__(256, 1) pass_v5_kernel(PassArgsV5 a)
                 if (!arrived) nbar_arrive(1, nthr);
                 nbar_sync(2, nw); // every A row done
                 TRACE5T(4);
+                TRACE5C(11);
                 v5_store<S, C>(Wg, ku, ldw1, n, c, t, q0, dq, p, W, Win, LA, tt, nw);
+                TRACE5C(12);
                 nbar_sync(2, nw);
                 if (tt == 0) {
+                    TRACE5C(13);
                     fence_acq_rel();
+                    TRACE5C(14);
                     st_release(pme, 2 * j + 1);
+                    TRACE5C(15);
                     TRACE5T(5);
                     // ------------------------------------------------ B half
                     if (pprev) wait_geq(pprev, min(2 * j + (j + 2 < Jp ? a.b0 : a.b0t), 2 * Jp));

@@ -98,12 +98,19 @@ struct PassArgsV6 {
     int *counter;
     unsigned long long *trace;
     int trace_groups, trace_steps;
+    int trace_ring; // slots 8..15 hold ring-latency clocks (writer / producer / WG0 / last WG) instead of step probes
 };
 
 #define TRACE6(slot_, j_)                                                                                  \
     do {                                                                                                   \
         if (a.trace && mat == 0 && k < a.trace_groups && (j_) < a.trace_steps)                            \
             a.trace[((int64_t)k * a.trace_steps + (j_)) * 16 + (slot_)] = gtimer();                        \
+    } while (0)
+// ring-latency probes (a.trace_ring): clock64 of one SM, slots 8..15
+#define TRACE6R(slot_, j_)                                                                                 \
+    do {                                                                                                   \
+        if (a.trace && a.trace_ring && mat == 0 && k < a.trace_groups && (j_) < a.trace_steps)            \
+            a.trace[((int64_t)k * a.trace_steps + (j_)) * 16 + (slot_)] = clock64();                       \
     } while (0)
 
 // ---- TMA (bulk tensor copies) ---------------------------------------------
@@ -188,7 +195,7 @@ __device__ __forceinline__ void step_v6(const PassArgsV6 &a, typename ComputeOf<
     }
     nbar_sync(bar, NT);
     if (tr && tid == 0) tr[g == 0 ? 4 : 7] = gtimer();
-#define PROBE6(i_) do { if (tr && tid == 0 && g == 0) tr[i_] = clock64(); } while (0)
+#define PROBE6(i_) do { if (tr && !a.trace_ring && tid == 0 && g == 0) tr[i_] = clock64(); } while (0)
     PROBE6(8);
 
     // ---------------------------------------------------------------- right application (A)
@@ -241,6 +248,7 @@ __device__ __forceinline__ void step_v6(const PassArgsV6 &a, typename ComputeOf<
     nbar_sync(bar, NT);
     if (tr && tid == 0 && g == 0) tr[5] = gtimer();
     PROBE6(12);
+    if (tr && a.trace_ring && tid == 0 && g == 0) tr[12] = clock64(); // WG0: chunk j+1 here
 
     // ---------------------------------------------------------------- left application (B)
     // y = A[p..hi][p], contiguous; columns p+1..ce, one per thread
@@ -418,6 +426,7 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v6_kernel(PassArgsV6 a, const _
                         step_v6_tail<S, MT>(a, ring, &xstage_s[g][0], r0, g, j, Jprev, y, tid, 1 + g, NT, tr);
                     if (g == 0 && tid == 0) TRACE6(6, j);
                     if (g == glast && tid == 0) TRACE6(1, j);
+                    if (g == glast && tid == 0) TRACE6R(13, j); // last WG finished step j
                 }
             }
         } else if ((int)threadIdx.x < ncomp + 32) {
@@ -430,6 +439,7 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v6_kernel(PassArgsV6 a, const _
                     // ring slot of chunk mm - R free (written back)
                     if (mm >= a.R)
                         while (wb_s < mm - a.R + 1) __nanosleep(64);
+                    TRACE6R(10, mm); // ring slot free
                     // the previous group's last sweep finished step mm + 1 (and wrote it back)
                     if (pprev) wait_geq_v4(pprev, min(2 * mm + 4, 2 * Jp), 2 * mm);
                     TRACE6(2, mm);
@@ -443,6 +453,7 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v6_kernel(PassArgsV6 a, const _
                         fence_proxy_async(); // acquired global data and freed slot -> async proxy
                         mb_expect_tx(fb, (unsigned)(c * P * sizeof(C)));
                         tma_load_3d(slot, &tmap, ku - (2 * MT - 1), x0, mat, fb);
+                        TRACE6R(11, mm); // load issued
                     }
                 } else {
                     __syncwarp();
@@ -498,6 +509,8 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v6_kernel(PassArgsV6 a, const _
                 }
                 have = __shfl_sync(0xffffffffu, have, 0);
                 const int jend = min(Js - 1, have >> 1); // steps [0, jend) of the last WG done
+                if (lane == 0)
+                    for (int jj = j; jj < jend; ++jj) TRACE6R(8, jj); // writer saw step jj done
                 for (; j < jend; ++j)
                     if (j < M) {
                         write_chunk(j);
@@ -507,6 +520,13 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v6_kernel(PassArgsV6 a, const _
                     if (lane == 0) {
                         tma_store_wait_read();
                         wb_s = wb; // slots free for the producer
+                        for (int jj = 0; jj < 64 && jend - 1 - jj >= 0; ++jj) {
+                            if (a.trace && a.trace_ring && mat == 0 && k < a.trace_groups && jend - 1 - jj < a.trace_steps) {
+                                unsigned long long *q = a.trace + ((int64_t)k * a.trace_steps + (jend - 1 - jj)) * 16 + 9;
+                                if (*q) break;
+                                *q = clock64(); // slot of chunk freed
+                            } else break;
+                        }
                     }
                 }
                 publish(2 * jend, wb);

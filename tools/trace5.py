@@ -31,3 +31,16 @@ def summarize(path):
 if __name__ == "__main__":
     for p in sys.argv[1:]:
         summarize(p)
+
+
+def wa_cycles(path):
+    """Cycle breakdown of the A write-back + publish (slots 11-15, clock64 of
+    thread 32): own stores issued, all warps' stores issued (barrier), fence,
+    release store."""
+    (ng, nu, c, t, G, grid), tr = read(path)
+    sl = tr[ng // 4: 3 * ng // 4, 2: nu - 2]
+    ok = (sl[:, :, 11] > 0) & (sl[:, :, 15] > 0)
+    for nm, a0, a1 in (("stores issued (own)", 11, 12), ("barrier (all warps issued)", 12, 13),
+                       ("fence.acq_rel.gpu", 13, 14), ("st.release.gpu", 14, 15)):
+        d = (sl[:, :, a1] - sl[:, :, a0])[ok]
+        print("  WA %-28s median %8.0f cycles  mean %8.0f" % (nm, np.median(d), np.mean(d)))

@@ -114,3 +114,33 @@ def crossgroup(path, k=2048, j0=400, nj=200):
     print(f"crossgroup k={k} G={G}: {len(rows)} steps")
     for i, nm in enumerate(names):
         print("  %-40s median %7.2f us  mean %7.2f" % (nm, np.nanmedian(a[:, i]), np.nanmean(a[:, i])))
+
+
+def ring(path, k=2048, j0=300, nj=400):
+    """Ring-latency probes (BB_TRACE_RING=1; clock64 of the group's SM, cycles):
+    last WG finished step m (13) -> writer saw it (8) -> slot freed after the
+    store read it (9) -> producer saw the free slot for chunk m+R (10) -> load
+    issued after the previous-group wait (11) -> WG0 past its B wait of step
+    m+R-1, i.e. chunk m+R usable (12)."""
+    (ng, ns, c, t, G, grid), tr = read(path)
+    R = None
+    # infer R: the smallest r with producer slot-free(m + r) >= slot freed(m) for most m
+    rows = {}
+    for r in range(2 * G + 1, 40):
+        d = tr[k, j0 + r: j0 + nj + r, 10] - tr[k, j0: j0 + nj, 9]
+        if np.median(d) > 0:
+            R = r
+            break
+    print(f"ring k={k} G={G} R~{R}")
+    if R is None:
+        return
+    m = np.arange(j0, j0 + nj)
+    s = tr[k]
+    parts = [("last WG done -> writer saw", s[m, 8] - s[m, 13]),
+             ("writer saw -> slot freed (store read)", s[m, 9] - s[m, 8]),
+             ("slot freed -> producer saw (chunk m+R)", s[m + R, 10] - s[m, 9]),
+             ("producer saw -> load issued (prev wait)", s[m + R, 11] - s[m + R, 10]),
+             ("load issued -> WG0 past B wait (j=m+R-1)", s[m + R - 1, 12] - s[m + R, 11]),
+             ("last WG done(m) -> WG0 past B wait(m+R-1)", s[m + R - 1, 12] - s[m, 13])]
+    for nm, d in parts:
+        print("  %-44s median %8.0f cycles  mean %8.0f" % (nm, np.median(d), np.mean(d)))
