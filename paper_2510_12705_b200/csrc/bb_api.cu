@@ -234,7 +234,11 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
                 const int cc = (int)c;
                 const int nt = 2 * cc;
                 const int ntmax = cs == 8 ? (cc == 32 ? 384 : 448) : (cc == 32 ? 512 : 576); // bb_launch.cuh instantiations
-                int gcap = 16;
+                // default cap 4: measured best for fp64 (the ring allows at most 4) and
+                // fp32 (n = 32768: 428 -> 395 ms, 16384: 183 -> 170, 8192: 74 -> 70,
+                // 1024: 6.8 -> 6.5 ms against the thread-bound G = 7,
+                // profiles/r02/v6_group_size_f32.txt); BB_V6_G overrides (up to 16)
+                int gcap = 4;
                 if (const char *e = getenv("BB_V6_G")) gcap = std::max(0, std::min(16, atoi(e)));
                 const size_t chunk = cs * (size_t)cc * (size_t)(3 * cc); // TMA box: 3c rows x c columns
                 const size_t budget = (size_t)kSmemOptinFallback - 10240; // static: barriers, counters, x staging
