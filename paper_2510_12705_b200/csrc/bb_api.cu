@@ -178,9 +178,10 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
                 // the unit window fits shared memory
                 int G = 0;
                 const int VP = (MT5 + 2) & ~1;
+                const bool wide = getenv("BB_V5_WIDE") != nullptr; // experiments: largest G <= c - t
                 if (ok5) {
                     for (int Gc : {32, 16, 8})
-                        if (Gc <= gcap && 2 * Gc <= c - t) {
+                        if (!wide && Gc <= gcap && 2 * Gc <= c - t) {
                             G = Gc;
                             break;
                         }
