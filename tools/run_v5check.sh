@@ -1,4 +1,4 @@
-# v5 change check: unit-kernel tests, headline timings, per-phase trace of pass 1
+# v5 change check: headline timings, config-3 timings, unit-kernel tests, per-phase trace of pass 1
 set -x
 timeout 300 python tools/quick_time.py f64 f32 > gpurun_out/v5check_qt.txt 2>&1
 timeout 250 python tools/maxb_sweep.py 8192 64 f64 32 0 >> gpurun_out/v5check_qt.txt 2>&1
