@@ -341,7 +341,7 @@ __device__ __forceinline__ void v5_axpy(C *__restrict__ own, const C *__restrict
 }
 
 template <class C, int MT, int GT>
-__device__ __forceinline__ void v5_panel(C *pan, int ks, int ls, C *vs, int VP, C * /*xb*/, int lane, C zero)
+__device__ __forceinline__ void v5_panel(C *pan, int ks, int ls, C *vs, int VP, C * /*xb*/, int lane)
 {
     // Only the member's own vector a[] lives in registers; the source x is
     // read from shared memory (broadcast) for the sums and again for the
@@ -370,12 +370,7 @@ __device__ __forceinline__ void v5_panel(C *pan, int ks, int ls, C *vs, int VP, 
         const C alpha = src[0];
         const C xl = (lane < MT) ? src[lane * ks] : C(0);
         const C x32 = (MT > 32) ? src[(MT > 32 ? 32 : 0) * ks] : C(0);
-        // the dot product enters the norm as s * zero (zero == 0 at run time, opaque
-        // to the compiler): without this ptxas scheduled the dot product's 8-deep
-        // DFMA chain AFTER the reflector scalars instead of beside the norm's
-        // (SASS); for finite s the sum is exactly the norm
-        const C sdot = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-        const C ss = fma(sdot, zero, (q4[0] + q4[1]) + (q4[2] + q4[3]));
+        const C ss = (q4[0] + q4[1]) + (q4[2] + q4[3]);
         C tau = 0, rho = 0, beta = alpha;
         bool nz = ss > C(0);
         if (!nz) { // rare: all squares underflowed or x[1:] == 0
@@ -394,7 +389,7 @@ __device__ __forceinline__ void v5_panel(C *pan, int ks, int ls, C *vs, int VP, 
             for (int k = 1; k < MT; ++k) s4[k & 3] = fma(a[k], v[k], s4[k & 3]);
         }
         if (upd && nz) {
-            const C w = tau * fma(rho, slow ? (s4[0] + s4[1]) + (s4[2] + s4[3]) : sdot, a[0]);
+            const C w = tau * fma(rho, (s4[0] + s4[1]) + (s4[2] + s4[3]), a[0]);
             const C wr = w * rho;
             own[0] = a[0] - w;
             if (!slow) {
@@ -457,7 +452,6 @@ __global__ void __launch_bounds__(256, 1) pass_v5_kernel(PassArgsV5 a)
     const int ku = a.ku;
     const int64_t ldw1 = (int64_t)a.ldw - 1;
     const int total = a.batch * a.ngroups;
-    const C zero = C(a.n < 0 ? 1 : 0); // 0, opaque (v5_panel)
 
     for (;;) {
         __syncthreads();
@@ -490,7 +484,7 @@ __global__ void __launch_bounds__(256, 1) pass_v5_kernel(PassArgsV5 a)
             }
             __syncthreads();
             TRACE5(2);
-            if (tid < 32) v5_panel<C, MT, GT>(Win, LA, 1, vA, VP, xbuf, lane, zero);
+            if (tid < 32) v5_panel<C, MT, GT>(Win, LA, 1, vA, VP, xbuf, lane);
             __syncthreads();
             TRACE5(3);
             // A bulk, split so that the B panel overlaps the rest of the A half:
@@ -538,7 +532,7 @@ __global__ void __launch_bounds__(256, 1) pass_v5_kernel(PassArgsV5 a)
                 TRACE5T(7);
             } else {
                 nbar_sync(1, nthr); // rows [p, p+W) of the A bulk done
-                v5_panel<C, MT, GT>(Win + dq, 1, LA, vB, VP, xbuf, lane, zero);
+                v5_panel<C, MT, GT>(Win + dq, 1, LA, vB, VP, xbuf, lane);
             }
             __syncthreads(); // B panel, H load and the whole A half complete
             TRACE5(8);
