@@ -112,6 +112,11 @@ typedef enum {
 #define BB_FLAG_NO_SEGMENT_KERNEL 0x8u /* never use the segment-ring kernel of the target-   */
                                        /* bandwidth-1 pass (bb_pass_v6.cuh); results are     */
                                        /* bitwise identical, for testing / comparison        */
+#define BB_FLAG_CHECK_ZEROS 0x10u /* debug: after the reduction, verify that every cell of the */
+                                  /* working band outside the diagonal and superdiagonal is   */
+                                  /* exactly zero (the structural zeros); SYNCHRONISES */
+                                  /* `stream`; BB_ERR_INTERNAL if any is not (d, e are still  */
+                                  /* written)                                                  */
 
 /* Tuning knobs, the paper's hyperparameter triple.
  * Zero-initialise for defaults. */

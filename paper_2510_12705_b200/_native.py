@@ -28,6 +28,7 @@ BB_FLAG_NONNEG_OUTPUT = 0x1
 BB_FLAG_GENERIC_KERNEL = 0x2
 BB_FLAG_NO_UNIT_KERNEL = 0x4
 BB_FLAG_NO_SEGMENT_KERNEL = 0x8
+BB_FLAG_CHECK_ZEROS = 0x10
 
 EXPORTED = [
     "bb_band_to_bidiag", "bb_band_to_bidiag_batched", "bb_band_to_bidiag_ex",

@@ -39,12 +39,14 @@ class Config:
     generic: bool = False       # force the generic shared-memory step kernel (testing)
     no_unit: bool = False       # never use the unit kernel (bb_pass_v5.cuh), for comparisons
     no_segment: bool = False    # never use the segment-ring kernel (bb_pass_v6.cuh), for comparisons
+    check_zeros: bool = False   # debug: verify the structural zeros on the device (synchronises)
     timing_events: tuple = ()   # torch.cuda.Event objects (enable_timing=True), >= passes + 3
 
     def c(self) -> N.bb_config:
         flags = ((N.BB_FLAG_NONNEG_OUTPUT if self.nonneg else 0) | (N.BB_FLAG_GENERIC_KERNEL if self.generic else 0)
                  | (N.BB_FLAG_NO_UNIT_KERNEL if self.no_unit else 0)
-                 | (N.BB_FLAG_NO_SEGMENT_KERNEL if self.no_segment else 0))
+                 | (N.BB_FLAG_NO_SEGMENT_KERNEL if self.no_segment else 0)
+                 | (N.BB_FLAG_CHECK_ZEROS if self.check_zeros else 0))
         cfg = N.bb_config(self.tw, self.threads_per_block, self.max_blocks_per_sm, self.dep_distance,
                           self.schedule, flags)
         if self.timing_events:

@@ -436,4 +436,32 @@ __global__ void extract_kernel(const S *__restrict__ W, int64_t mat_stride, int 
     }
 }
 
+// ---- BB_FLAG_CHECK_ZEROS (debug) --------------------------------------------
+// Count the working-band cells outside the diagonal and the superdiagonal that
+// are not exactly zero after the reduction (the structural zeros of P:308 /
+// BASELINE north_star; reading Q11): every cell of the n x ldw storage of each
+// matrix, A(i, j) = W[(ku + i - j) + j*ldw], except offsets j - i in {0, 1}
+// (padding cells, rows outside [0, n), are zero from the pack kernel on).
+__device__ __forceinline__ bool cell_nonzero(float v) { return v != 0.f; }
+__device__ __forceinline__ bool cell_nonzero(double v) { return v != 0.0; }
+__device__ __forceinline__ bool cell_nonzero(__half v) { return __half2float(v) != 0.f; }
+template <class S>
+__global__ void check_zeros_kernel(const S *__restrict__ W, int64_t mat_stride, int ldw, int ku, int n, int batch,
+                                   int *__restrict__ count)
+{
+    const int64_t per = (int64_t)n * ldw;
+    const int64_t total = per * batch;
+    int local = 0;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t mat = idx / per;
+        const int64_t rem = idx - mat * per;
+        const int r = (int)(rem % ldw);
+        const int off = ku - r; // j - i
+        if (off == 0 || off == 1) continue;
+        local += cell_nonzero(W[mat * mat_stride + rem]) ? 1 : 0;
+    }
+    if (local) atomicAdd(count, local);
+}
+
 } // namespace bb

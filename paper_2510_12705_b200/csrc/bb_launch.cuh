@@ -463,6 +463,18 @@ bb_status launch_all(const Plan &P, const void *band, int64_t ldband, int64_t st
     }
     mark(2 + (int)P.passes.size());
     if (cudaGetLastError() != cudaSuccess) return BB_ERR_CUDA;
+    if (P.cfg.flags & BB_FLAG_CHECK_ZEROS) { // debug: structural zeros exact? (synchronises the stream)
+        int64_t total = (int64_t)batch * n * P.ldw;
+        int thr = 256;
+        int64_t blocks = std::min<int64_t>((total + thr - 1) / thr, (int64_t)di.sms * 8);
+        if (cudaMemsetAsync(counters, 0, sizeof(int), st) != cudaSuccess) return BB_ERR_CUDA;
+        bb::check_zeros_kernel<S><<<(unsigned)std::max<int64_t>(blocks, 1), thr, 0, st>>>(
+            W, mat_stride, (int)P.ldw, (int)P.ku, n, batch, counters);
+        int h = 0;
+        if (cudaMemcpyAsync(&h, counters, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess) return BB_ERR_CUDA;
+        if (cudaStreamSynchronize(st) != cudaSuccess) return BB_ERR_CUDA;
+        if (h != 0) return BB_ERR_INTERNAL;
+    }
     return BB_SUCCESS;
 }
 

@@ -147,3 +147,15 @@ def test_svals_validation_is_synchronous():
     assert L.bb_bidiag_svals(0, N.BB_F64, None, None, None, None, 0, None) == N.BB_SUCCESS
     assert L.bb_bidiag_svals_batched(10, N.BB_F64, 2, fake, 5, fake, 9, fake, 10, fake, 1 << 20,
                                      None) == N.BB_ERR_INVALID_VALUE   # overlapping d strides
+
+
+def test_header_flag_constants_match_binding():
+    # every BB_FLAG_* / BB_SCHED_* value the header defines is the binding's value
+    import re
+    from paper_2510_12705_b200 import _native as N
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
+                            "bandbidiag.h")).read()
+    defs = dict(re.findall(r"#define\s+(BB_(?:FLAG|SCHED)_[A-Z_]+)\s+(0x[0-9a-fA-F]+|\d+)u?", hdr))
+    assert "BB_FLAG_CHECK_ZEROS" in defs
+    for name, val in defs.items():
+        assert getattr(N, name) == int(val, 0), name

@@ -95,3 +95,29 @@ def test_guard_bands_and_poisoned_workspace(n, b, dtype, tw, batch, kw):
     for x, y in ((d0, d1), (e0, e1), (d0, d2), (e0, e2)):
         assert torch.equal(x.view(torch.uint8), y.view(torch.uint8))
     assert torch.isfinite(d0.double()).all() and torch.isfinite(e0.double()).all()
+
+
+@pytest.mark.parametrize("n,b,dtype,tw,kw", [(777, 128, "f64", 32, {}), (901, 64, "f32", 32, {}),
+                                             (513, 64, "f16", 16, {}), (600, 64, "f64", 32, {"no_unit": True}),
+                                             (333, 40, "f64", 7, {}), (300, 40, "f32", 16, {"generic": True})])
+def test_check_zeros_flag(n, b, dtype, tw, kw):
+    # BB_FLAG_CHECK_ZEROS: the device-side structural-zero check passes on every
+    # kernel family and leaves (d, e) identical to the unchecked call
+    bb = _bb()
+    from tests.gpu_util import gpu_reduce
+    band = synth.random_band(n, b, dtype, seed=44)
+    ref = gpu_reduce(band, b, cfg=bb.Config(tw=tw, **kw))
+    got = gpu_reduce(band, b, cfg=bb.Config(tw=tw, check_zeros=True, **kw))
+    assert np.array_equal(ref[0], got[0]) and np.array_equal(ref[1], got[1])
+
+
+def test_check_zeros_flag_detects_incomplete_reduction(monkeypatch):
+    # only the first of three passes run (debug knob): the band is not bidiagonal
+    bb = _bb()
+    from paper_2510_12705_b200 import _native as N
+    from tests.gpu_util import gpu_reduce
+    band = synth.random_band(500, 96, "f64", seed=45)
+    monkeypatch.setenv("BB_DEBUG_PASSES", "1")
+    with pytest.raises(N.BBError) as ex:
+        gpu_reduce(band, 96, cfg=bb.Config(tw=32, check_zeros=True))
+    assert ex.value.status == N.BB_ERR_INTERNAL
