@@ -281,8 +281,7 @@ __device__ __forceinline__ void step_v6(const PassArgsV6 &a, typename ComputeOf<
     }
 }
 
-// clipped steps (matrix end) and steps whose row access wraps the ring: out of
-// line, so the hot code (full, non-wrapping step) stays small
+// clipped steps (matrix end): out of line, so the hot code stays small
 template <class S, int MT>
 __device__ __noinline__ void step_v6_tail(const PassArgsV6 &a, typename ComputeOf<S>::type *ring,
                                           typename ComputeOf<S>::type *xstage, int r0, int g, int j, int Jprev,
@@ -422,6 +421,10 @@ __global__ void __launch_bounds__(NTMAX, 1) pass_v6_kernel(PassArgsV6 a, const _
                                                  : nullptr;
                     if (full && xb + MT <= NB)
                         step_v6<S, MT, true, false>(a, ring, &xstage_s[g][0], r0, g, j, Jprev, y, tid, 1 + g, NT, tr);
+                    else if (full) // the row access wraps the ring (once per R steps for WG g > 0): inline,
+                                   // an out-of-line call saved / restored ~600 B of registers per thread
+                                   // through local memory
+                        step_v6<S, MT, true, true>(a, ring, &xstage_s[g][0], r0, g, j, Jprev, y, tid, 1 + g, NT, tr);
                     else
                         step_v6_tail<S, MT>(a, ring, &xstage_s[g][0], r0, g, j, Jprev, y, tid, 1 + g, NT, tr);
                     if (g == 0 && tid == 0) TRACE6(6, j);
