@@ -242,7 +242,16 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
                 int gcap = 4;
                 if (const char *e = getenv("BB_V6_G")) gcap = std::max(0, std::min(16, atoi(e)));
                 const size_t chunk = cs * (size_t)cc * (size_t)(3 * cc); // TMA box: 3c rows x c columns
-                const size_t budget = (size_t)kSmemOptinFallback - 10240; // static: barriers, counters, x staging
+                // ring budget: the 196 KB shared-memory carve-out (static: barriers, counters,
+                // x staging ~10 KB) -- the kernel is measurably faster with >= 60 KB of L1 left
+                // than at the 228 KB carve-out (fp64, c = 32: G = 3 / R = 7 at 181 KB: 297 ms,
+                // G = 3 / R = 8 at 206 KB: 312 ms, G = 4 / R = 9 at 230 KB: 309 ms;
+                // profiles/r02/v6_group_ring_sweep.txt); falls back to the full opt-in size
+                const size_t budget_l1 = (size_t)196 * 1024 - 10240;
+                const size_t budget_max = (size_t)kSmemOptinFallback - 10240;
+                const bool env_g = getenv("BB_V6_G") != nullptr; // experiments / tests ask for a group size
+                for (size_t budget : {env_g ? budget_max : budget_l1, budget_max}) {
+                if (pp.g6 > 0) break;
                 for (int G = std::min(std::min(gcap, 14), cc); G >= 1; --G) { // named barriers 1 + g <= 15; G <= c
                     // (the writer's finality rule, tests/test_v6_protocol.py)
                     if (G * nt + 64 > ntmax) continue;
@@ -260,6 +269,7 @@ bb_status make_plan(int64_t n, int64_t b, bb_dtype dtype, int64_t batch, const b
                     pp.smem6 = (size_t)R * chunk + 128; // + alignment of the ring to 128 bytes
                     pp.ngroups6 = (int)((ns + G - 1) / G);
                     break;
+                }
                 }
             }
             P.passes.push_back(pp);
